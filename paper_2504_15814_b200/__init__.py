@@ -1,0 +1,50 @@
+"""B200-native halo interpolation / restriction for 3:1 AMR patch faces.
+
+Drop-in for the hot path of the reference package ``trihalo``
+(/root/reference/pkg/src/trihalo/__init__.py:6-53): the operator API
+(interpolate_halo, restrict_halo, apply_scheme, HaloExchange,
+scheme_feasible, build_reference_operator, operator caches), its geometry
+types and its exception classes.  The arithmetic runs in sm_100a CUDA
+kernels behind the C ABI of include/trihalo_b200.h; operators are built on
+the host in C++ and uploaded once per (role, scheme, p, k).  Batched,
+device-resident faces go through ``faces.FaceBatch``.
+"""
+
+from .errors import (
+    ConfigurationError,
+    ContractViolationError,
+    DeviceError,
+    SingularFitError,
+    StencilInfeasibleError,
+    TrihaloError,
+)
+from .geometry import (
+    DEFAULT_UNKNOWNS,
+    FaceConfig,
+    HaloBuffer,
+    RegionShape,
+    ReferenceFrame,
+    from_reference,
+    gather_cell_indices,
+    interp_source_shape,
+    interp_target_shape,
+    reference_frame,
+    restrict_source_shape,
+    restrict_target_shape,
+    to_reference,
+)
+from .operators import CsrOperator, DeviceOperator, OperatorCache, OperatorKey, apply, operator_cache_get
+from .schemes import (
+    MATRIX_SCHEMES,
+    SCHEMES,
+    HaloExchange,
+    apply_scheme,
+    build_reference_operator,
+    interpolate_halo,
+    require_feasible,
+    restrict_halo,
+    scheme_feasible,
+)
+from .faces import FaceBatch, pool_interp_faces, pool_restrict_faces, slab_faces
+
+__version__ = "0.1.0"

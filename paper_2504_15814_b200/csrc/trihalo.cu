@@ -1,0 +1,551 @@
+// B200 (sm_100a) kernels and the C ABI of include/trihalo_b200.h.
+//
+// Data model: AoS cells (u unknowns contiguous, the reference HaloBuffer
+// layout, geometry.py:272-303) addressed through per-face offsets/strides.
+// Each warp owns one (face, block) work item: a block is the tensor product
+// of one normal group and two tangential groups of the operator (see
+// builder.hpp) — a source window of <= 5x5x5 cells feeding <= 27 target
+// cells.  Lanes run over unknowns (lane, lane+32), so every weight is
+// warp-uniform (one broadcast load feeds 2 unknowns x 2 children) and every
+// source/target cell access is a contiguous 8*u-byte run (coalesced for all
+// six face orientations; the orientation only changes strides).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/trihalo_b200.h"
+#include "builder.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_last_column = -1;
+
+int32_t fail(int32_t code, const std::string& msg, int col = -1) {
+  g_last_error = msg;
+  g_last_column = col;
+  return code;
+}
+
+#define TH_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) return fail(TH_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device view of an operator (passed by value)
+// ---------------------------------------------------------------------------
+struct DevOp {
+  int32_t role, scheme, p, k;
+  int32_t ns0;         // source extent along the normal (2k)
+  int32_t G0, G1;      // groups along normal / tangential
+  int32_t max_items;   // work items per face (upper bound)
+  const int4* grp0;    // (win0, winL, tgt0, tgtN)
+  const int4* grp1;
+  const int32_t* block_id;
+  const int64_t* block_off;
+  const int32_t* block_cp;
+  const double* weights;
+  const int64_t* row_off0;  // 1-D rows (tensor_linear)
+  const double* rows0;
+  const int64_t* row_off1;
+  const double* rows1;
+  int32_t seg_g[3][2];
+  int32_t half_g[3][2];
+  int32_t half_t[3][2];
+};
+
+// one face, rewritten in reference-frame terms: source cell (a0, a1, a2) of
+// block b lives at src[b] + a0*sn + (a1 - b1*p)*s1 + (a2 - b2*p)*s2 and target
+// cell (t0, t1, t2) at dst + (t0-lo0)*dn + (t1-lo1)*d1 + (t2-lo2)*d2; the
+// normal flip of geometry.py:180-190 is folded into the signed strides.
+struct FaceRef {
+  int64_t src0;   // block 0 (interpolation)
+  int64_t sn, s1, s2;
+  int64_t dst, dn, d1, d2;
+  int lo0, lo1, lo2, hi0;
+  int g0, n0, g1, n1, g2, n2;
+};
+
+__device__ __forceinline__ void decode_face(const th_face* __restrict__ fp, const DevOp& op, FaceRef& r) {
+  const int n = __ldg(&fp->normal);
+  const int side = __ldg(&fp->side);
+  const int t1 = (n == 0) ? 1 : 0, t2 = (n == 2) ? 1 : 2;
+  const int64_t ssn = __ldg(&fp->src_stride[n]);
+  r.s1 = __ldg(&fp->src_stride[t1]);
+  r.s2 = __ldg(&fp->src_stride[t2]);
+  r.sn = side ? -ssn : ssn;
+  const int64_t sadj = side ? int64_t(op.ns0 - 1) * ssn : 0;
+  r.src0 = __ldg(&fp->src[0]) + sadj;
+  const int64_t dsn = __ldg(&fp->dst_stride[n]);
+  r.d1 = __ldg(&fp->dst_stride[t1]);
+  r.d2 = __ldg(&fp->dst_stride[t2]);
+  int box0;
+  if (op.role == 0) {
+    const int s = __ldg(&fp->segment);
+    r.lo0 = 0;
+    r.hi0 = op.k;
+    r.lo1 = (s % 3) * op.p;
+    r.lo2 = (s / 3) * op.p;
+    r.g0 = 0;
+    r.n0 = op.G0;
+    r.g1 = op.seg_g[s % 3][0];
+    r.n1 = op.seg_g[s % 3][1] - r.g1;
+    r.g2 = op.seg_g[s / 3][0];
+    r.n2 = op.seg_g[s / 3][1] - r.g2;
+    box0 = op.k;
+  } else {
+    const int h = __ldg(&fp->half);
+    r.lo0 = op.half_t[h][0];
+    r.hi0 = op.half_t[h][1];
+    r.lo1 = r.lo2 = 0;
+    r.g0 = op.half_g[h][0];
+    r.n0 = op.half_g[h][1] - r.g0;
+    r.g1 = r.g2 = 0;
+    r.n1 = r.n2 = op.G1;
+    box0 = r.hi0 - r.lo0;
+  }
+  r.dn = side ? -dsn : dsn;
+  r.dst = __ldg(&fp->dst) + (side ? int64_t(box0 - 1) * dsn : 0);
+}
+
+// source address of reference source cell (a0, a1, a2) (relative to lane 0)
+__device__ __forceinline__ int64_t src_addr(const th_face* __restrict__ fp, const DevOp& op, const FaceRef& r,
+                                            int a0, int a1, int a2) {
+  if (op.role == 0) return r.src0 + a0 * r.sn + a1 * r.s1 + a2 * r.s2;
+  const int b1 = a1 / op.p, b2 = a2 / op.p;
+  const int64_t base = __ldg(&fp->src[b1 + 3 * b2]) + (r.src0 - __ldg(&fp->src[0]));
+  return base + a0 * r.sn + (a1 - b1 * op.p) * r.s1 + (a2 - b2 * op.p) * r.s2;
+}
+
+__device__ __forceinline__ bool decode_item(const DevOp& op, const FaceRef& fr, int it, int& g0, int& g1, int& g2) {
+  const int n12 = fr.n1 * fr.n2;
+  if (it >= fr.n0 * n12) return false;
+  g1 = fr.g1 + it % fr.n1;
+  const int r = it / fr.n1;
+  g2 = fr.g2 + r % fr.n2;
+  g0 = fr.g0 + r / fr.n2;
+  return true;
+}
+
+__device__ __forceinline__ void raise_flag(int32_t* flag, bool bad) {
+  if (flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// generic dense-block apply: out[child] = sum_cell W[cell][child] * v[cell]
+// ---------------------------------------------------------------------------
+template <int MAXC>
+__global__ void __launch_bounds__(128) dense_apply_kernel(DevOp op, const double* __restrict__ src,
+                                                          double* __restrict__ dst,
+                                                          const th_face* __restrict__ faces, int64_t n_faces,
+                                                          int u, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = n_faces * op.max_items;
+  for (int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; item < total; item += nwarps) {
+    const int64_t f = item / op.max_items;
+    const int it = int(item - f * op.max_items);
+    const th_face* fp = faces + f;
+    FaceRef fr;
+    decode_face(fp, op, fr);
+    int g0, g1, g2;
+    if (!decode_item(op, fr, it, g0, g1, g2)) continue;
+    const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]), G2 = __ldg(&op.grp1[g2]);
+    const int bid = __ldg(&op.block_id[(g0 * op.G1 + g1) * op.G1 + g2]);
+    const double* __restrict__ W = op.weights + __ldg(&op.block_off[bid]);
+    const int CP = __ldg(&op.block_cp[bid]);
+    const int C0 = G0.w, C1 = G1.w, C = G0.w * G1.w * G2.w;
+    for (int cb = 0; cb < u; cb += 64) {
+      const bool ok0 = cb + lane < u, ok1 = cb + lane + 32 < u;
+      double acc[MAXC][2];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) acc[c][0] = acc[c][1] = 0.0;
+      int cell = 0;
+      for (int z = 0; z < G2.y; ++z)
+        for (int y = 0; y < G1.y; ++y) {
+          const int64_t row = src_addr(fp, op, fr, G0.x, G1.x + y, G2.x + z) + cb + lane;
+          for (int x = 0; x < G0.y; ++x, ++cell) {
+            const double* sp = src + row + int64_t(x) * fr.sn;
+            const double v0 = ok0 ? __ldg(sp) : 0.0;
+            const double v1 = ok1 ? __ldg(sp + 32) : 0.0;
+            const double2* wc = reinterpret_cast<const double2*>(W + int64_t(cell) * CP);
+#pragma unroll
+            for (int c = 0; c < MAXC; c += 2) {
+              if (c < C) {
+                const double2 w = __ldg(wc + c / 2);
+                acc[c][0] = fma(w.x, v0, acc[c][0]);
+                acc[c][1] = fma(w.x, v1, acc[c][1]);
+                acc[c + 1][0] = fma(w.y, v0, acc[c + 1][0]);
+                acc[c + 1][1] = fma(w.y, v1, acc[c + 1][1]);
+              }
+            }
+          }
+        }
+      bool bad = false;
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        if (c < C) {
+          const int i0 = c % C0, i1 = (c / C0) % C1, i2 = c / (C0 * C1);
+          const int t0 = G0.z + i0, t1 = G1.z + i1, t2 = G2.z + i2;
+          if (t0 >= fr.lo0 && t0 < fr.hi0 && t1 >= fr.lo1 && t1 < fr.lo1 + op.p && t2 >= fr.lo2 &&
+              t2 < fr.lo2 + op.p) {
+            double* dp = dst + fr.dst + (t0 - fr.lo0) * fr.dn + (t1 - fr.lo1) * fr.d1 + (t2 - fr.lo2) * fr.d2 +
+                         cb + lane;
+            if (ok0) { dp[0] = acc[c][0]; bad |= !isfinite(acc[c][0]); }
+            if (ok1) { dp[32] = acc[c][1]; bad |= !isfinite(acc[c][1]); }
+          }
+        }
+      }
+      raise_flag(flag, bad);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// d-linear tensor product: three per-axis passes (normal, t1, t2) over the
+// block window, in the reference's contraction order (linear.py:115-151)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const double* __restrict__ src,
+                                                           double* __restrict__ dst,
+                                                           const th_face* __restrict__ faces, int64_t n_faces,
+                                                           int u, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = n_faces * op.max_items;
+  for (int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; item < total; item += nwarps) {
+    const int64_t f = item / op.max_items;
+    const int it = int(item - f * op.max_items);
+    const th_face* fp = faces + f;
+    FaceRef fr;
+    decode_face(fp, op, fr);
+    int g0, g1, g2;
+    if (!decode_item(op, fr, it, g0, g1, g2)) continue;
+    const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]), G2 = __ldg(&op.grp1[g2]);
+    const double* __restrict__ R0 = op.rows0 + __ldg(&op.row_off0[g0]);  // [C0][L0]
+    const double* __restrict__ R1 = op.rows1 + __ldg(&op.row_off1[g1]);  // [C1][L1]
+    const double* __restrict__ R2 = op.rows1 + __ldg(&op.row_off1[g2]);  // [C2][L2]
+    for (int cb = 0; cb < u; cb += 64) {
+      const bool ok0 = cb + lane < u, ok1 = cb + lane + 32 < u;
+      double out[3][3][3][2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) out[a][b][c][0] = out[a][b][c][1] = 0.0;
+      for (int z = 0; z < G2.y; ++z) {
+        double tyz[3][3][2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) tyz[a][b][0] = tyz[a][b][1] = 0.0;
+        for (int y = 0; y < G1.y; ++y) {
+          const int64_t row = src_addr(fp, op, fr, G0.x, G1.x + y, G2.x + z) + cb + lane;
+          double tx[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+          for (int x = 0; x < G0.y; ++x) {
+            const double* sp = src + row + int64_t(x) * fr.sn;
+            const double v0 = ok0 ? __ldg(sp) : 0.0;
+            const double v1 = ok1 ? __ldg(sp + 32) : 0.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+              if (a < G0.w) {
+                const double w = __ldg(R0 + a * G0.y + x);
+                tx[a][0] = fma(w, v0, tx[a][0]);
+                tx[a][1] = fma(w, v1, tx[a][1]);
+              }
+          }
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            if (b < G1.w) {
+              const double w = __ldg(R1 + b * G1.y + y);
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                tyz[a][b][0] = fma(w, tx[a][0], tyz[a][b][0]);
+                tyz[a][b][1] = fma(w, tx[a][1], tyz[a][b][1]);
+              }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c < G2.w) {
+            const double w = __ldg(R2 + c * G2.y + z);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) {
+                out[a][b][c][0] = fma(w, tyz[a][b][0], out[a][b][c][0]);
+                out[a][b][c][1] = fma(w, tyz[a][b][1], out[a][b][c][1]);
+              }
+          }
+      }
+      bool bad = false;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (a < G0.w && b < G1.w && c < G2.w) {
+              const int t0 = G0.z + a, t1 = G1.z + b, t2 = G2.z + c;
+              if (t0 >= fr.lo0 && t0 < fr.hi0 && t1 >= fr.lo1 && t1 < fr.lo1 + op.p && t2 >= fr.lo2 &&
+                  t2 < fr.lo2 + op.p) {
+                double* dp = dst + fr.dst + (t0 - fr.lo0) * fr.dn + (t1 - fr.lo1) * fr.d1 +
+                             (t2 - fr.lo2) * fr.d2 + cb + lane;
+                if (ok0) { dp[0] = out[a][b][c][0]; bad |= !isfinite(out[a][b][c][0]); }
+                if (ok1) { dp[32] = out[a][b][c][1]; bad |= !isfinite(out[a][b][c][1]); }
+              }
+            }
+          }
+      raise_flag(flag, bad);
+    }
+  }
+}
+
+__global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
+  bool bad = false;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    bad |= !isfinite(__ldg(v + i));
+  raise_flag(flag, bad);
+}
+
+// csr._apply_kernel (csr.py:143-156): one warp per row, lanes over unknowns
+__global__ void csr_apply_kernel(const int64_t* __restrict__ ro, const int64_t* __restrict__ ci,
+                                 const double* __restrict__ val, int64_t n_rows, const double* __restrict__ src,
+                                 double* __restrict__ out, int u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nwarps) {
+    const int64_t lo = __ldg(ro + r), hi = __ldg(ro + r + 1);
+    for (int cb = 0; cb < u; cb += 32) {
+      if (cb + lane >= u) break;
+      double acc = 0.0;
+      for (int64_t t = lo; t < hi; ++t) acc = fma(__ldg(val + t), __ldg(src + __ldg(ci + t) * u + cb + lane), acc);
+      out[r * u + cb + lane] = acc;
+    }
+  }
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+struct th_operator {
+  th::HostOperator host;
+  DevOp dev;
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  int max_children = 0;
+  bool on_device = false;
+};
+
+namespace {
+
+template <class T>
+int32_t upload(th_operator* op, const std::vector<T>& v, const T** out) {
+  if (v.empty()) { *out = nullptr; return TH_OK; }
+  void* p = nullptr;
+  TH_CUDA(cudaMalloc(&p, v.size() * sizeof(T)));
+  op->allocs.push_back(p);
+  TH_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  op->bytes += int64_t(v.size() * sizeof(T));
+  *out = static_cast<const T*>(p);
+  return TH_OK;
+}
+
+int32_t map_error(const th::Error& e) {
+  return fail(int32_t(e.code), e.what(), e.column);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t th_abi_version(void) { return 1; }
+
+const char* th_last_error(void) { return g_last_error.c_str(); }
+
+int32_t th_last_error_column(void) { return g_last_column; }
+
+int32_t th_scheme_feasible(int32_t role, int32_t scheme, int32_t p, int32_t k) {
+  try {
+    th::check_feasible(role, scheme, p, k);
+  } catch (const th::Error& e) {
+    return map_error(e);
+  }
+  return TH_OK;
+}
+
+void th_operator_destroy(th_operator* op) {
+  if (!op) return;
+  for (void* p : op->allocs) cudaFree(p);
+  delete op;
+}
+
+static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t k, th_operator** out,
+                               bool upload_to_device) {
+  if (!out) return fail(TH_ERR_CONFIG, "out pointer is NULL");
+  *out = nullptr;
+  th_operator* op = new th_operator();
+  try {
+    op->host = th::build_operator(role, scheme, p, k);
+  } catch (const th::Error& e) {
+    delete op;
+    return map_error(e);
+  } catch (const std::exception& e) {
+    delete op;
+    return fail(TH_ERR_CONFIG, e.what());
+  }
+  const th::HostOperator& h = op->host;
+  DevOp& d = op->dev;
+  std::memset(&d, 0, sizeof(d));
+  d.role = h.role;
+  d.scheme = h.scheme;
+  d.p = h.p;
+  d.k = h.k;
+  d.ns0 = h.ax[0].ns;
+  d.G0 = (int)h.groups[0].size();
+  d.G1 = (int)h.groups[1].size();
+  d.max_items = h.max_items;
+  std::memcpy(d.seg_g, h.seg_g, sizeof(d.seg_g));
+  std::memcpy(d.half_g, h.half_g, sizeof(d.half_g));
+  std::memcpy(d.half_t, h.half_t, sizeof(d.half_t));
+  std::vector<int4> g0, g1;
+  for (const auto& g : h.groups[0]) {
+    g0.push_back(make_int4(g.win0, g.winL, g.tgt0, g.tgtN));
+    op->max_children = std::max(op->max_children, g.tgtN);
+  }
+  int mc1 = 0;
+  for (const auto& g : h.groups[1]) {
+    g1.push_back(make_int4(g.win0, g.winL, g.tgt0, g.tgtN));
+    mc1 = std::max(mc1, g.tgtN);
+  }
+  op->max_children *= mc1 * mc1;
+  op->on_device = upload_to_device;
+  if (!upload_to_device) {
+    *out = op;
+    return TH_OK;
+  }
+  int32_t rc;
+  if ((rc = upload(op, g0, &d.grp0)) || (rc = upload(op, g1, &d.grp1)) || (rc = upload(op, h.block_id, &d.block_id)) ||
+      (rc = upload(op, h.block_off, &d.block_off)) || (rc = upload(op, h.block_cp, &d.block_cp)) ||
+      (rc = upload(op, h.weights, &d.weights)) || (rc = upload(op, h.row_off[0], &d.row_off0)) ||
+      (rc = upload(op, h.rows[0], &d.rows0)) || (rc = upload(op, h.row_off[1], &d.row_off1)) ||
+      (rc = upload(op, h.rows[1], &d.rows1))) {
+    th_operator_destroy(op);
+    return rc;
+  }
+  *out = op;
+  return TH_OK;
+}
+
+int32_t th_operator_create(int32_t role, int32_t scheme, int32_t p, int32_t k, th_operator** out) {
+  return operator_create(role, scheme, p, k, out, true);
+}
+
+int32_t th_operator_create_host(int32_t role, int32_t scheme, int32_t p, int32_t k, th_operator** out) {
+  return operator_create(role, scheme, p, k, out, false);
+}
+
+int32_t th_operator_info_get(const th_operator* op, th_operator_info* info) {
+  if (!op || !info) return fail(TH_ERR_CONFIG, "NULL operator or info");
+  const th::HostOperator& h = op->host;
+  info->role = h.role;
+  info->scheme = h.scheme;
+  info->p = h.p;
+  info->k = h.k;
+  info->n_src_cells = h.n_src_cells();
+  info->n_tgt_cells_full = h.n_tgt_cells();
+  info->n_blocks = (int32_t)h.block_off.size();
+  info->max_items_per_face = h.max_items;
+  info->device_bytes = op->bytes;
+  info->max_condition = h.max_condition;
+  info->n_condition_warnings = h.n_condition_warnings;
+  info->kernel = h.scheme == TH_SCHEME_TENSOR_LINEAR ? 1 : 0;
+  return TH_OK;
+}
+
+int32_t th_operator_export_rows(const th_operator* op, int32_t selector, int64_t* n_rows, int64_t* nnz,
+                                int64_t* row_offsets, int64_t* col_indices, double* values) {
+  if (!op || !n_rows || !nnz) return fail(TH_ERR_CONFIG, "NULL argument");
+  std::vector<int64_t> ro, ci;
+  std::vector<double> v;
+  try {
+    th::export_rows(op->host, selector, ro, ci, v);
+  } catch (const th::Error& e) {
+    return map_error(e);
+  }
+  *n_rows = int64_t(ro.size()) - 1;
+  *nnz = int64_t(ci.size());
+  if (row_offsets) std::memcpy(row_offsets, ro.data(), ro.size() * sizeof(int64_t));
+  if (col_indices) std::memcpy(col_indices, ci.data(), ci.size() * sizeof(int64_t));
+  if (values) std::memcpy(values, v.data(), v.size() * sizeof(double));
+  return TH_OK;
+}
+
+int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, const th_face* faces, int64_t n_faces,
+                       int32_t u, int32_t* flag, void* stream) {
+  if (!op) return fail(TH_ERR_CONFIG, "NULL operator");
+  if (!op->on_device) return fail(TH_ERR_CONTRACT, "operator was built host-only (th_operator_create_host)");
+  if (u < 1) return fail(TH_ERR_CONFIG, "u must be >= 1, got " + std::to_string(u));
+  if (n_faces < 0) return fail(TH_ERR_CONFIG, "n_faces must be >= 0");
+  if (n_faces == 0) return TH_OK;
+  if (!src || !dst || !faces) return fail(TH_ERR_CONTRACT, "NULL source, target or face pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t items = n_faces * int64_t(op->dev.max_items);
+  const int threads = 128;
+  const int64_t want = (items + 3) / 4;
+  const int blocks = int(std::min<int64_t>(want, int64_t(num_sms()) * 16));
+  if (op->dev.scheme == TH_SCHEME_TENSOR_LINEAR) {
+    tensor_apply_kernel<<<blocks, threads, 0, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  } else if (op->max_children <= 4) {
+    dense_apply_kernel<4><<<blocks, threads, 0, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  } else if (op->max_children <= 10) {
+    dense_apply_kernel<10><<<blocks, threads, 0, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  } else {
+    dense_apply_kernel<28><<<blocks, threads, 0, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  }
+  TH_CUDA(cudaGetLastError());
+  return TH_OK;
+}
+
+int32_t th_check_finite(const double* values, int64_t n, int32_t* flag, void* stream) {
+  if (n <= 0) return TH_OK;
+  if (!values || !flag) return fail(TH_ERR_CONTRACT, "NULL pointer");
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+  finite_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(values, n, flag);
+  TH_CUDA(cudaGetLastError());
+  return TH_OK;
+}
+
+int32_t th_csr_apply(const int64_t* row_offsets, const int64_t* col_indices, const double* values, int64_t n_rows,
+                     const double* src, double* out, int32_t u, void* stream) {
+  if (u < 1) return fail(TH_ERR_CONFIG, "u must be >= 1");
+  if (n_rows <= 0) return TH_OK;
+  const int blocks = int(std::min<int64_t>((n_rows + 3) / 4, int64_t(num_sms()) * 16));
+  csr_apply_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(row_offsets, col_indices, values, n_rows,
+                                                                         src, out, u);
+  TH_CUDA(cudaGetLastError());
+  return TH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerance: norm-wise relative error per face max|gpu - ref| / max|ref| <= 1e-12
+(BASELINE.json north star, fp64).  Index maps are exercised bit-exactly by the
+golden comparison (a wrong gather / scatter shows up as O(1) error).
+"""
+
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+FACES = list(itertools.product(("x", "y", "z"), ("negative", "positive")))
+
+
+@pytest.fixture(scope="module")
+def th():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_15814_b200 as th
+
+    return th
+
+
+def rel(a, b):
+    scale = np.abs(b).max() if b.size else 1.0
+    return float(np.abs(a - b).max() / max(scale, 1e-300)) if a.size else 0.0
+
+
+def oracle_run(cfg, scheme, role, half, src):
+    from oracle import exchange as OE
+    from oracle import geometry as OG
+
+    ocfg = OG.FaceCfg(cfg.normal_axis, cfg.coarse_side, cfg.segment, cfg.p, cfg.k, cfg.u)
+    ex = OE.OracleExchange(ocfg, scheme, role, half)
+    out = np.empty(ex.n_out)
+    ex.run(src, out)
+    return out
+
+
+SMALL = [(4, 3, 3), (5, 2, 2), (6, 3, 5), (3, 3, 2), (1, 1, 2), (2, 2, 3), (4, 1, 1), (5, 3, 59), (5, 3, 70)]
+
+
+@pytest.mark.parametrize("p,k,u", SMALL)
+@pytest.mark.parametrize("scheme", ("tensor_linear", "matrix_linear", "order2", "order3"))
+def test_exchange_all_faces_small(th, p, k, u, scheme):
+    rng = np.random.default_rng(p * 100 + k * 10 + u)
+    checked = 0
+    for (normal, side), role_half in itertools.product(FACES, (("interpolate", None), ("restrict", None),
+                                                              ("restrict", "inner"), ("restrict", "outer"))):
+        role, half = role_half
+        ok, _ = th.scheme_feasible(scheme, role, p, k)
+        if not ok:
+            continue
+        segs = range(9) if role == "interpolate" else (0,)
+        for seg in segs:
+            cfg = th.FaceConfig(normal, side, seg, p, k, u)
+            ex = th.HaloExchange(cfg, scheme, role, half=half)
+            src, out = ex.make_buffers(rng)
+            ex.run(src, out)
+            want = oracle_run(cfg, scheme, role, half, src)
+            assert rel(out, want) <= TOL, (scheme, role, half, normal, side, seg, rel(out, want))
+            checked += 1
+    if checked == 0:
+        pytest.skip("scheme infeasible at this (p, k) for both roles")
+
+
+def test_golden_exchange_outputs(th):
+    """Reference HaloExchange.run outputs captured in tests/golden/exchange.npz."""
+    import os
+
+    data = np.load(os.path.join(os.path.dirname(__file__), "golden", "exchange.npz"))
+    keys = sorted({k.rsplit("|", 1)[0] for k in data.files})
+    worst = 0.0
+    for key in keys:
+        scheme, role, half, p, k, u, normal, side, seg = key.split("|")
+        half = None if half == "None" else half
+        p, k, u, seg = int(p), int(k), int(u), int(seg)
+        cfg = th.FaceConfig(normal, side, seg, p, k, u)
+        ex = th.HaloExchange(cfg, scheme, role, half=half)
+        src = np.random.default_rng(int(data[key + "|seed"][0])).standard_normal(ex.n_src)
+        out = np.zeros(ex.n_out)
+        ex.run(src, out)
+        err = rel(out, data[key + "|out"])
+        worst = max(worst, err)
+        assert err <= TOL, (key, err)
+    assert len(keys) > 500
+
+
+def test_functional_api_matches_exchange(th):
+    rng = np.random.default_rng(3)
+    for scheme in th.SCHEMES:
+        cfg = th.FaceConfig("z", "positive", 7, 9, 3, 59)
+        src_region = th.interp_source_shape(cfg)
+        buf = th.HaloBuffer(src_region, 59, rng.standard_normal(src_region.cell_count * 59))
+        got = th.interpolate_halo(cfg, scheme, buf)
+        assert got.region == th.interp_target_shape(cfg)
+        assert rel(got.values, oracle_run(cfg, scheme, "interpolate", None, buf.values)) <= TOL
+        fr = th.restrict_source_shape(cfg)
+        fb = th.HaloBuffer(fr, 59, rng.standard_normal(fr.cell_count * 59))
+        for half in (None, "inner", "outer"):
+            got = th.apply_scheme(cfg, scheme, "restrict", fb, half=half)
+            assert got.region == th.restrict_target_shape(cfg, half)
+            assert rel(got.values, oracle_run(cfg, scheme, "restrict", half, fb.values)) <= TOL
+
+
+def test_nonfinite_source_raises(th):
+    cfg = th.FaceConfig("x", "negative", 0, 4, 3, 2)
+    ex = th.HaloExchange(cfg, "order2", "interpolate")
+    src, out = ex.make_buffers(np.random.default_rng(0))
+    src[5] = np.nan
+    with pytest.raises(th.ContractViolationError):
+        ex.run(src, out)
+    src[5] = 0.0
+    src[-1] = np.inf  # outside the operator support still counts (schemes.py:186)
+    with pytest.raises(th.ContractViolationError):
+        ex.run(src, out)
+    src[-1] = 0.0
+    ex.run(src, out)  # flag was cleared
+
+
+def test_wrong_region_raises(th):
+    cfg = th.FaceConfig("x", "negative", 0, 4, 3, 2)
+    wrong = th.HaloBuffer.zeros(th.restrict_source_shape(cfg), 2)
+    with pytest.raises(th.ContractViolationError):
+        th.interpolate_halo(cfg, "matrix_linear", wrong)
+    with pytest.raises(th.StencilInfeasibleError):
+        th.HaloExchange(th.FaceConfig("x", "negative", 0, 4, 1, 1), "order2", "interpolate")
+
+
+def test_csr_apply_matches_dense(th):
+    """csr.apply on the device vs a dense product (reference test_csr.py:79-89 analogue)."""
+    rng = np.random.default_rng(1)
+    op = th.build_reference_operator("order3", "interpolate", 5, 3, segment=4)
+    src = th.HaloBuffer(op.source_region, 58, rng.standard_normal(op.n_cols * 58))
+    got = th.apply(op, src).values.reshape(op.n_rows, 58)
+    want = op.to_dense() @ src.values.reshape(op.n_cols, 58)
+    assert np.abs(got - want).max() < 1e-13 * max(1.0, np.abs(want).max())
+
+
+# ---------------------------------------------------------------------------
+# batched faces: slab and pool layouts
+# ---------------------------------------------------------------------------
+
+def _world_box(pool, E, u, pid, lo, ext):
+    """Extract a world box (x-fastest AoS) from pool patch `pid`: lo/ext per world axis."""
+    g = pool[pid].reshape(E, E, E, u)  # (z, y, x, u)
+    return np.ascontiguousarray(g[lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]]).reshape(-1)
+
+
+def _interp_box(p, k, normal, side):
+    """Independent derivation of the coarse-patch box feeding interpolation."""
+    lo, ext = [k, k, k], [p, p, p]
+    lo[normal] = p if side == 0 else 0
+    ext[normal] = 2 * k
+    return lo, ext
+
+
+@pytest.mark.parametrize("scheme", ("tensor_linear", "matrix_linear", "order2", "order3"))
+@pytest.mark.parametrize("p", (9, 17))
+def test_pool_interp_batch(th, scheme, p):
+    import torch
+
+    k, u = 3, 59
+    rng = np.random.default_rng(p)
+    E = p + 2 * k
+    n_patch, n_face = 6, 40
+    pool = rng.standard_normal((n_patch, E ** 3 * u))
+    cid = rng.integers(0, n_patch, n_face)
+    nrm = rng.integers(0, 3, n_face)
+    sid = rng.integers(0, 2, n_face)
+    seg = rng.integers(0, 9, n_face)
+    rec = th.pool_interp_faces(p, k, u, cid, nrm, sid, seg)
+    op = th.operators.DEFAULT_CACHE.device_operator("interpolate", scheme, p, k)
+    batch = th.FaceBatch(op, rec, u)
+    dev = torch.device("cuda")
+    src = torch.from_numpy(pool.reshape(-1)).to(dev)
+    dst = torch.full((n_face * k * p * p * u,), np.nan, dtype=torch.float64, device=dev)
+    batch.launch(src, dst)
+    out = dst.cpu().numpy().reshape(n_face, -1)
+    assert not batch.nonfinite()
+    for f in range(n_face):
+        lo, ext = _interp_box(p, k, int(nrm[f]), int(sid[f]))
+        box = _world_box(pool, E, u, int(cid[f]), lo, ext)
+        cfg = th.FaceConfig("xyz"[nrm[f]], ("negative", "positive")[sid[f]], int(seg[f]), p, k, u)
+        want = oracle_run(cfg, scheme, "interpolate", None, box)
+        assert rel(out[f], want) <= TOL, (f, rel(out[f], want))
+
+
+@pytest.mark.parametrize("scheme", ("tensor_linear", "matrix_linear", "order2", "order3"))
+@pytest.mark.parametrize("p,half", ((9, None), (17, None), (9, "inner"), (9, "outer")))
+def test_pool_restrict_batch(th, scheme, p, half):
+    import torch
+
+    k, u = 3, 59
+    rng = np.random.default_rng(p + 7)
+    E = p + 2 * k
+    n_patch, n_face = 12, 16
+    pool = rng.standard_normal((n_patch, E ** 3 * u))
+    nrm = rng.integers(0, 3, n_face)
+    sid = rng.integers(0, 2, n_face)
+    fine = rng.integers(0, n_patch, (n_face, 9))
+    rec = th.pool_restrict_faces(p, k, u, fine, nrm, sid, half=half)
+    op = th.operators.DEFAULT_CACHE.device_operator("restrict", scheme, p, k)
+    batch = th.FaceBatch(op, rec, u)
+    dev = torch.device("cuda")
+    src = torch.from_numpy(pool.reshape(-1)).to(dev)
+    lo_h, hi_h = th.geometry.half_layers(k, half)
+    ncell = (hi_h - lo_h) * p * p
+    dst = torch.full((n_face * ncell * u,), np.nan, dtype=torch.float64, device=dev)
+    batch.launch(src, dst)
+    out = dst.cpu().numpy().reshape(n_face, -1)
+    for f in range(n_face):
+        n = int(nrm[f])
+        t1, t2 = [d for d in range(3) if d != n]
+        # assemble the world restriction source (2k x 3p x 3p) from the nine fine patches
+        ext = [3 * p, 3 * p, 3 * p]
+        ext[n] = 2 * k
+        world = np.zeros((ext[2], ext[1], ext[0], u))
+        for b in range(9):
+            b1, b2 = b % 3, b // 3
+            lo = [k, k, k]
+            lo[n] = 0 if sid[f] == 0 else p
+            e = [p, p, p]
+            e[n] = 2 * k
+            blk = _world_box(pool, E, u, int(fine[f, b]), lo, e).reshape(e[2], e[1], e[0], u)
+            off = [0, 0, 0]
+            off[t1], off[t2] = b1 * p, b2 * p
+            world[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = blk
+        cfg = th.FaceConfig("xyz"[n], ("negative", "positive")[sid[f]], 0, p, k, u)
+        want = oracle_run(cfg, scheme, "restrict", half, world.reshape(-1))
+        assert rel(out[f], want) <= TOL, (f, rel(out[f], want))
+
+
+def test_restrict_into_coarse_halo(th):
+    """Restriction written straight into the coarse patches' halo layers of the pool."""
+    import torch
+
+    p, k, u = 9, 3, 5
+    rng = np.random.default_rng(11)
+    E = p + 2 * k
+    fine_pool = rng.standard_normal((9, E ** 3 * u))
+    coarse_pool = np.zeros((2, E ** 3 * u))
+    dev = torch.device("cuda")
+    for half in (None, "inner", "outer"):
+        rec = th.pool_restrict_faces(p, k, u, np.arange(9)[None, :].repeat(2, 0), [1, 2], [0, 1], half=half,
+                                     coarse_ids=[0, 1])
+        rec_slab = th.pool_restrict_faces(p, k, u, np.arange(9)[None, :].repeat(2, 0), [1, 2], [0, 1], half=half)
+        op = th.operators.DEFAULT_CACHE.device_operator("restrict", "order2", p, k)
+        src = torch.from_numpy(fine_pool.reshape(-1)).to(dev)
+        cdst = torch.from_numpy(coarse_pool.reshape(-1)).to(dev)
+        th.FaceBatch(op, rec, u).launch(src, cdst)
+        lo_h, hi_h = th.geometry.half_layers(k, half)
+        sdst = torch.zeros(2 * (hi_h - lo_h) * p * p * u, dtype=torch.float64, device=dev)
+        th.FaceBatch(op, rec_slab, u).launch(src, sdst)
+        slab = sdst.cpu().numpy().reshape(2, -1)
+        cp = cdst.cpu().numpy().reshape(2, E, E, E, u)
+        for f, (n, side) in enumerate(((1, 0), (2, 1))):
+            lo, ext = [k, k, k], [p, p, p]
+            lo[n] = p + k + lo_h if side == 0 else k - hi_h
+            ext[n] = hi_h - lo_h
+            box = cp[f, lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]].reshape(-1)
+            assert np.array_equal(box, slab[f])
