@@ -1,0 +1,471 @@
+"""Benchmark of the B200 halo interpolation / restriction path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one pass of every (role, scheme) of BASELINE.json's config over all
+of its faces, inputs resident in HBM.  Default: config 2 (configs[1]): p=9,
+k=3, u=59, 1,024 coarse patches, 4,096 faces; tensor_linear + order2
+interpolation and tensor_linear + order2 restriction (full coarse face) of
+every face.  Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine ghost-cell values/s (interp+restrict, fp64) and % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 6 and parts[0].isdigit():
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes / flops per face (distinct support cells + output)
+# ---------------------------------------------------------------------------
+
+def unit_costs(role, scheme, p, k, u, selectors):
+    """Per-face (bytes, flops) averaged over the faces' segments / halves, from the
+    operator's exported rows (the reference CSR structure)."""
+    from paper_2504_15814_b200.operators import HostOperator
+
+    h = HostOperator(role, scheme, p, k)
+    cache = {}
+    b_tot = f_tot = 0.0
+    for sel in selectors:
+        if sel not in cache:
+            c = h.csr(segment=int(sel)) if role == "interpolate" else h.csr(half=sel)
+            support = np.unique(c.col_indices).size
+            cache[sel] = ((support + c.n_rows) * u * 8.0, 2.0 * c.nnz * u)
+        b, f = cache[sel]
+        b_tot += b
+        f_tot += f
+    n = max(1, len(selectors))
+    return b_tot / n, f_tot / n, h.info.device_bytes if hasattr(h.info, "device_bytes") else 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2504_15814_b200 as th
+    import workloads as W
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    wl = W.build(args.config, rank=rank)
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    passes = []
+    cache = th.operators.DEFAULT_CACHE
+    for role, scheme in s.passes:
+        op = cache.device_operator(role, scheme, p, k)
+        if role == "interpolate":
+            rec, src, ids = W.interp_records(wl), wl.pool, wl.interp_ids
+            n_tgt = k * p * p
+            sel = wl.faces.segment[ids]
+        else:
+            rec, src, ids = W.restrict_records(wl), wl.fine, wl.restrict_ids
+            n_tgt = k * p * p
+            sel = [None] * ids.size
+        batch = th.FaceBatch(op, rec, u)
+        out = torch.empty(ids.size * n_tgt * u, dtype=torch.float64, device=dev)
+        b, f, _ = unit_costs(role, scheme, p, k, u, sel)
+        passes.append(dict(role=role, scheme=scheme, batch=batch, src=src, out=out, n=ids.size,
+                           values=ids.size * n_tgt * u, bytes=b * ids.size + op.info.device_bytes,
+                           flops=f * ids.size))
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        for i, ps in enumerate(passes):
+            if evs is not None:
+                evs[i].record(stream)
+            ps["batch"].launch(ps["src"], ps["out"], check_flag=False)
+        if evs is not None:
+            evs[-1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.05)
+    ev_all = [[torch.cuda.Event(enable_timing=True) for _ in range(len(passes) + 1)] for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for kk in range(args.steps):
+        step(ev_all[kk])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    total_ms = t0.elapsed_time(t1)
+    per_pass_ms = [statistics.mean(ev[i].elapsed_time(ev[i + 1]) for ev in ev_all) for i in range(len(passes))]
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    values_per_step = sum(ps["values"] for ps in passes)
+    value = values_per_step * world / (ms_per_step / 1e3)
+    peak, peak_kind = peaks()
+    pass_rows = []
+    for ps, ms in zip(passes, per_pass_ms):
+        gbs = ps["bytes"] / (ms / 1e3) / 1e9
+        pass_rows.append({"role": ps["role"], "scheme": ps["scheme"], "faces": ps["n"], "ms": round(ms, 4),
+                          "alg_bytes": int(ps["bytes"]), "alg_GBps": round(gbs, 1), "frac_hbm": round(gbs / peak, 3),
+                          "fp64_TFLOPs": round(ps["flops"] / (ms / 1e3) / 1e12, 2)})
+    dom = max(range(len(passes)), key=lambda i: per_pass_ms[i])
+    result = {
+        "metric": METRIC, "value": value, "unit": "values/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded field (BASELINE config text) sampled at cell centres + 1e-6 N(0,1), generated in HBM",
+        "config": {"workload": f"config{s.config}: {s.name}", "p": p, "k": k, "u": u, "coarse_patches": s.n_patches,
+                   "faces": s.n_faces, "passes": [f"{r}:{sc}" for r, sc in s.passes],
+                   "layout": "coarse pool (p+2k)^3 AoS + per-face fine restriction slabs (world layout)",
+                   "l2": f"inputs {(wl.pool.numel() + (wl.fine.numel() if wl.fine is not None else 0)) * 8 / 1e9:.1f} GB"
+                         " >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"weak: {world} independent shard(s)"},
+        "roofline": {"bound": "hbm", "kernel": f"{passes[dom]['role']}:{passes[dom]['scheme']}",
+                     "achieved": pass_rows[dom]["alg_GBps"], "peak": peak, "unit": "GB/s",
+                     "frac": round(pass_rows[dom]["alg_GBps"] / peak, 4), "traffic": None,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"},
+        "passes": pass_rows,
+        "gpu_launches": args.steps * len(passes),
+        "clocks": clocks,
+    }
+    step_bytes = sum(ps["bytes"] for ps in passes)
+    result["step_alg_GBps"] = round(step_bytes / (ms_per_step / 1e3) / 1e9, 1)
+    result["step_frac_hbm"] = round(step_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4)
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, wl, passes, dev, world)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"], result["parity"] = cpu_baseline(args, wl, passes)
+    return result
+
+
+def run_e2e(args, wl, passes, dev, world):
+    """Same metric through the C ABI with HOST buffers: every step copies each face's
+    reference source buffer (pinned host -> HBM), applies all passes, copies the results
+    back; chunked over 3 streams so PCIe traffic overlaps the kernels."""
+    import torch
+
+    import paper_2504_15814_b200 as th
+    import workloads as W
+
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    # host copies of the per-face reference source buffers
+    n_i, n_r = wl.interp_ids.size, wl.restrict_ids.size
+    per_i, per_r = 2 * k * p * p * u, 2 * k * 9 * p * p * u
+    h_i = torch.empty(n_i * per_i, dtype=torch.float64, pin_memory=True)
+    for a in range(0, n_i, 1024):
+        b = min(n_i, a + 1024)
+        h_i[a * per_i:b * per_i].copy_(W.interp_source_boxes(wl, wl.interp_ids[a:b]).reshape(-1))
+    h_r = torch.empty(max(1, n_r * per_r), dtype=torch.float64, pin_memory=True)
+    if n_r:
+        h_r.copy_(wl.fine)
+    d_i = torch.empty(max(1, n_i * per_i), dtype=torch.float64, device=dev)
+    d_r = torch.empty(max(1, n_r * per_r), dtype=torch.float64, device=dev)
+    n_chunks = 8
+    chunks = []
+    outs_h = []
+    fc = wl.faces
+    for ps in passes:
+        outs_h.append(torch.empty(ps["out"].numel(), dtype=torch.float64, pin_memory=True))
+    for c in range(n_chunks):
+        ia, ib = n_i * c // n_chunks, n_i * (c + 1) // n_chunks
+        ra, rb = n_r * c // n_chunks, n_r * (c + 1) // n_chunks
+        batches = []
+        for ps in passes:
+            op = ps["batch"].op
+            if ps["role"] == "interpolate":
+                ids = wl.interp_ids[ia:ib]
+                rec = th.slab_faces("interpolate", p, k, u, fc.normal[ids], fc.side[ids], segments=fc.segment[ids],
+                                    src_offsets=np.arange(ia, ib) * per_i,
+                                    dst_offsets=np.arange(ia, ib) * k * p * p * u)
+                lo, hi = ia, ib
+            else:
+                ids = wl.restrict_ids[ra:rb]
+                rec = th.slab_faces("restrict", p, k, u, fc.normal[ids], fc.side[ids],
+                                    src_offsets=np.arange(ra, rb) * per_r,
+                                    dst_offsets=np.arange(ra, rb) * k * p * p * u)
+                lo, hi = ra, rb
+            batches.append((th.FaceBatch(op, rec, u) if hi > lo else None, lo, hi))
+        chunks.append(dict(ia=ia, ib=ib, ra=ra, rb=rb, batches=batches))
+    s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    tgt = k * p * p * u
+
+    def e2e_step():
+        for ch in chunks:
+            with torch.cuda.stream(s_in):
+                if ch["ib"] > ch["ia"]:
+                    d_i[ch["ia"] * per_i:ch["ib"] * per_i].copy_(h_i[ch["ia"] * per_i:ch["ib"] * per_i], non_blocking=True)
+                if ch["rb"] > ch["ra"]:
+                    d_r[ch["ra"] * per_r:ch["rb"] * per_r].copy_(h_r[ch["ra"] * per_r:ch["rb"] * per_r], non_blocking=True)
+                e_in = torch.cuda.Event()
+                e_in.record(s_in)
+            s_run.wait_event(e_in)
+            with torch.cuda.stream(s_run):
+                for ps, (batch, lo, hi) in zip(passes, ch["batches"]):
+                    if batch is not None:
+                        batch.launch(d_i if ps["role"] == "interpolate" else d_r, ps["out"], check_flag=False)
+                e_run = torch.cuda.Event()
+                e_run.record(s_run)
+            s_out.wait_event(e_run)
+            with torch.cuda.stream(s_out):
+                for ps, oh, (batch, lo, hi) in zip(passes, outs_h, ch["batches"]):
+                    if hi > lo:
+                        oh[lo * tgt:hi * tgt].copy_(ps["out"][lo * tgt:hi * tgt], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(max(1, args.e2e_steps)):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        e2e_step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t)
+    t_step = statistics.median(times)
+    if world > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    values = sum(ps["values"] for ps in passes) * world
+    return {"value": values / t_step, "unit": "values/s",
+            "h2d_bytes_per_step": int((n_i * per_i + n_r * per_r) * 8),
+            "d2h_bytes_per_step": int(sum(ps["out"].numel() for ps in passes) * 8),
+            "ms_per_step": round(t_step * 1e3, 2),
+            "how": "pinned host buffers of the per-face reference source layouts -> th_apply_faces -> pinned host "
+                   "outputs, 8 chunks pipelined over copy/compute/copy streams; wall clock with device sync"}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(args, wl, passes):
+    """Oracle port (C restatement of the reference HaloExchange.run) on a sample of
+    this workload's faces, on the host cores; also a parity check of our outputs."""
+    import torch
+
+    import workloads as W
+    from oracle import exchange as OE
+    from oracle import geometry as OG
+
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    rng = np.random.default_rng(12345)
+    nth = cpu_threads()
+    jobs = []
+    fc = wl.faces
+    sample_i = rng.choice(wl.interp_ids, min(args.cpu_sample, wl.interp_ids.size), replace=False) \
+        if wl.interp_ids.size else np.zeros(0, dtype=np.int64)
+    sample_r = rng.choice(np.arange(wl.restrict_ids.size), min(args.cpu_sample, wl.restrict_ids.size),
+                          replace=False) if wl.restrict_ids.size else np.zeros(0, dtype=np.int64)
+    per_r = 2 * k * 9 * p * p * u
+    tgt = k * p * p * u
+    src_i = W.interp_source_boxes(wl, sample_i).cpu().numpy() if sample_i.size else None
+    worst = 0.0
+    values = 0
+    for ps in passes:
+        outs_dev = ps["out"]
+        if ps["role"] == "interpolate":
+            pos = {f: i for i, f in enumerate(wl.interp_ids)}
+            for j, f in enumerate(sample_i):
+                cfg = OG.FaceCfg("xyz"[fc.normal[f]], ("negative", "positive")[fc.side[f]], int(fc.segment[f]), p, k, u)
+                ex = OE.exchange_for(cfg, ps["scheme"], "interpolate")
+                got = outs_dev[pos[f] * tgt:(pos[f] + 1) * tgt].cpu().numpy()
+                jobs.append((ex, src_i[j], np.empty(ex.n_out), got))
+        else:
+            for j in sample_r:
+                f = wl.restrict_ids[j]
+                cfg = OG.FaceCfg("xyz"[fc.normal[f]], ("negative", "positive")[fc.side[f]], 0, p, k, u)
+                ex = OE.exchange_for(cfg, ps["scheme"], "restrict")
+                src = wl.fine[j * per_r:(j + 1) * per_r].cpu().numpy()
+                got = outs_dev[j * tgt:(j + 1) * tgt].cpu().numpy()
+                jobs.append((ex, src, np.empty(ex.n_out), got))
+    t = time.perf_counter()
+    status = OE.run_many([j[0] for j in jobs], [j[1] for j in jobs], [j[2] for j in jobs], nth)
+    dt = time.perf_counter() - t
+    assert (status == 0).all()
+    for ex, src, want, got in jobs:
+        values += want.size
+        worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))
+    base = {"value": values / dt, "unit": "values/s", "cores": nth, "kind": "port",
+            "sample": f"{len(jobs)} face-passes ({sample_i.size} interp faces x interp passes + {sample_r.size} "
+                      f"restrict faces x restrict passes) of this workload; oracle C restatement of "
+                      f"HaloExchange.run over {nth} OpenMP threads; {dt:.2f} s"}
+    parity = {"sample_face_passes": len(jobs), "max_rel_err": worst, "tol": 1e-12, "ok": worst <= 1e-12}
+    return base, parity
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path (oracle port; the reference is Python
+# and cannot travel to the GPU box) on the host cores, same config and metric
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    import workloads as W
+    from oracle import exchange as OE
+    from oracle import geometry as OG
+
+    wl = W.describe(args.config)
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    rng = np.random.default_rng(777)
+    nth = cpu_threads()
+    n_sample = min(args.cpu_sample, s.n_faces)
+    fc = wl.faces
+    jobs = []
+    for role, scheme in s.passes:
+        ids = wl.interp_ids if role == "interpolate" else wl.restrict_ids
+        pick = np.sort(rng.choice(ids, min(n_sample, ids.size), replace=False))
+        for f in pick:
+            seg = int(fc.segment[f]) if role == "interpolate" else 0
+            cfg = OG.FaceCfg("xyz"[fc.normal[f]], ("negative", "positive")[fc.side[f]], seg, p, k, u)
+            ex = OE.exchange_for(cfg, scheme, role)
+            jobs.append((ex, W.host_sources(wl, int(f), role, rng), np.empty(ex.n_out)))
+    exs, srcs, outs = zip(*jobs)
+
+    def step():
+        st = OE.run_many(exs, srcs, outs, nth)
+        assert (st == 0).all()
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t) / args.steps
+    values = sum(o.size for o in outs)
+    value = values / dt
+    sample = (f"{len(jobs)} face-passes per step ({n_sample} faces per pass) drawn from config{s.config}; "
+              f"oracle C restatement of HaloExchange.run (reference schemes.py:185-202) over {nth} OpenMP threads")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "values/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator, host numpy)",
+            "config": {"workload": f"config{s.config}: {s.name}", "p": p, "k": k, "u": u,
+                       "passes": [f"{r}:{sc}" for r, sc in s.passes]},
+            "cpu_baseline": {"value": value, "unit": "values/s", "cores": nth, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "values/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
