@@ -231,6 +231,61 @@ Win taylor_window(int c, int ns, int block) {
   return {st, L};
 }
 
+// Discrete orthogonal (Gram) polynomials on the centred window points
+// {-1,0,1} / {-2,...,2}, integer-valued there: the least-squares fit of
+// taylor.py over a full tensor window equals the orthogonal projection onto
+// total degree <= order, whatever basis spans that space, so the kernels
+// project with these (diagonal normal matrix) instead of applying A+.
+double gram_value(int L, int a, double e) {
+  switch (a) {
+    case 0: return 1.0;
+    case 1: return e;
+    case 2: return L == 3 ? 3.0 * e * e - 2.0 : e * e - 2.0;
+  }
+  return (5.0 * e * e * e - 17.0 * e) / 6.0;
+}
+
+double gram_norm(int L, int a) {
+  static const double n3[3] = {3.0, 2.0, 6.0};
+  static const double n5[4] = {5.0, 10.0, 14.0, 10.0};
+  return L == 3 ? n3[a] : n5[a];
+}
+
+void choose_fast_path(HostOperator& op) {
+  const bool interp = op.role == 0;
+  const int L = op.scheme == 3 ? 5 : 3;
+  const int C0 = 3, CT = interp ? 3 : 1;
+  auto axis_ok = [&](const std::vector<Group>& gr, int Lw, int Cmax) {
+    for (const Group& g : gr)
+      if (g.winL != Lw || g.tgtN > Cmax) return false;
+    return true;
+  };
+  if (!axis_ok(op.groups[0], L, C0) || !axis_ok(op.groups[1], L, CT)) return;
+  op.fast_L0 = op.fast_LT = L;
+  op.fast_C0 = C0;
+  op.fast_CT = CT;
+  if (op.scheme == 0) {
+    op.fast_mode = 2;
+  } else if (interp && op.scheme >= 2) {
+    op.fast_mode = 3;
+    const int order = op.scheme;
+    for (int a = 0; a < 2; ++a) {
+      const AxisGeom& g = op.ax[a];
+      for (const Group& gr : op.groups[a]) {
+        const double mid = g.src_level(gr.win0 + (L - 1) / 2);
+        for (int c = 0; c < 3; ++c)
+          for (int d = 0; d < 4; ++d) {
+            double v = 0.0;
+            if (c < gr.tgtN && d <= order) v = gram_value(L, d, (g.tgt_level(gr.tgt0 + c) - mid) / g.s_sp) / gram_norm(L, d);
+            op.synth[a].push_back(v);
+          }
+      }
+    }
+  } else {
+    op.fast_mode = 1;
+  }
+}
+
 }  // namespace
 
 void check_feasible(int role, int scheme, int p, int k) {
@@ -450,6 +505,7 @@ HostOperator build_operator(int role, int scheme, int p, int k) {
     }
   }
   if (!taylor) op.max_condition = std::nan("");
+  choose_fast_path(op);
   return op;
 }
 

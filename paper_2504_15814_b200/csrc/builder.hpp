@@ -62,6 +62,13 @@ struct HostOperator {
   int half_g[3][2] = {};  // normal group range of half h (interpolation: all)
   int half_t[3][2] = {};  // normal target index range of half h
   int max_items = 0;
+  // fast fixed-window kernels (trihalo.cu window_kernel): every normal group
+  // has window fast_L0 and <= fast_C0 children, every tangential group
+  // window fast_LT and <= fast_CT children
+  int fast_mode = 0;  // 0 none, 1 dense blocks, 2 tensor rows, 3 Gram-separable least squares
+  int fast_L0 = 0, fast_LT = 0, fast_C0 = 0, fast_CT = 0;
+  // Gram synthesis values per group: [child < 3][degree < 4] = P_a(e_child) / |P_a|^2
+  std::vector<double> synth[2];
   double max_condition = 0.0;
   int n_condition_warnings = 0;
   std::vector<std::string> condition_warnings;
