@@ -282,6 +282,12 @@ void choose_fast_path(HostOperator& op) {
       }
     }
   } else {
+    // dense blocks are laid out with the real child counts: the fixed-window
+    // kernel indexes them as C0 x CT x CT, so every group must be full
+    for (const Group& g : op.groups[0])
+      if (g.tgtN != C0) return;
+    for (const Group& g : op.groups[1])
+      if (g.tgtN != CT) return;
     op.fast_mode = 1;
   }
 }

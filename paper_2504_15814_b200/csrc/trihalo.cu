@@ -812,7 +812,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
   else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0);
   else if (h.fast_mode == 2 && h.fast_L0 == 3 && interp) TH_WIN(2, 3, 3, 0, 1, 0);
-  else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 1, 0);
+  else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 2, 0);
   else if (h.fast_mode == 1 && h.fast_L0 == 3 && interp) TH_WIN(1, 3, 3, 0, 2, 0);
   else if (h.fast_mode == 1 && h.fast_L0 == 3 && !interp && op->smem_ok) TH_WIN(1, 3, 1, 0, 2, op->smem_bytes);
   else if (h.fast_mode == 1 && h.fast_L0 == 5 && !interp && op->smem_ok) TH_WIN(1, 5, 1, 0, 2, op->smem_bytes);
