@@ -59,6 +59,7 @@ struct DevOp {
   const double* synth0;     // Gram synthesis tables [group][3][4]
   const double* synth1;
   int32_t n_blocks;
+  int32_t units_per_face;   // (normal group, t1 group) columns per face, fixed-window kernels
   int32_t seg_g[3][2];
   int32_t half_g[3][2];
   int32_t half_t[3][2];
@@ -311,277 +312,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
   }
 }
 
-// ---------------------------------------------------------------------------
-// fixed-window kernels (the hot path at k = 3): every group of the operator
-// has a window of exactly L0 (normal) / LT (tangential) cells and at most
-// C0 / CT children.  Each warp loads its block's window one tangential line
-// (L0 cells along the normal) at a time, all lines of a z-slice in flight.
-//   MODE 1  dense weights W[cell][child] (restriction: children <= 4 staged in
-//           shared memory and shared by NU = 2 unknowns per lane)
-//   MODE 2  tensor_linear: three 1-D passes in the reference's order
-//           (normal, t1, t2; linear.py:115-151)
-//   MODE 3  order2 / order3 least squares as an orthogonal projection onto
-//           total degree <= ORDER with the discrete Gram polynomials of the
-//           window (integer weights: moments are adds), then the separable
-//           evaluation at the children (synthesis tables from the builder)
-// ---------------------------------------------------------------------------
-template <int L>
-struct Gram;
-template <>
-struct Gram<3> {  // {-1, 0, 1}: 1 | x | 3x^2 - 2
-  static constexpr int D = 3;
-  __device__ static constexpr double P(int a, int x) {
-    return a == 0 ? 1.0 : a == 1 ? double(x - 1) : (x == 1 ? -2.0 : 1.0);
-  }
-};
-template <>
-struct Gram<5> {  // {-2..2}: 1 | x | x^2 - 2 | (5x^3 - 17x) / 6
-  static constexpr int D = 4;
-  __device__ static constexpr double P(int a, int x) {
-    return a == 0 ? 1.0
-         : a == 1 ? double(x - 2)
-         : a == 2 ? double((x - 2) * (x - 2) - 2)
-                  : (x == 0 ? -1.0 : x == 1 ? 2.0 : x == 2 ? 0.0 : x == 3 ? -2.0 : 1.0);
-  }
-};
-
-// runtime Gram value at integer window offset z (for the non-unrolled slice loop)
-template <int L>
-__device__ __forceinline__ double gram_rt(int a, int z) {
-  const double t = double(z - (L - 1) / 2);
-  if (a == 0) return 1.0;
-  if (a == 1) return t;
-  if (a == 2) return L == 3 ? 3.0 * t * t - 2.0 : t * t - 2.0;
-  return (5.0 * t * t * t - 17.0 * t) / 6.0;
-}
-
-template <int MODE, int L0, int LT, int C0, int CT, int ORDER, int NU>
-__global__ void __launch_bounds__(128) window_kernel(DevOp op, const double* __restrict__ src,
-                                                     double* __restrict__ dst, const th_face* __restrict__ faces,
-                                                     int64_t n_faces, int u, int32_t* flag) {
-  constexpr int S = L0 * LT * LT;
-  constexpr int CH = C0 * CT * CT;
-  constexpr bool SMEM_W = (MODE == 1 && CH <= 4);
-  extern __shared__ double4 sw4[];
-  if constexpr (SMEM_W) {
-    const double4* gw = reinterpret_cast<const double4*>(op.weights);
-    for (int i = threadIdx.x; i < op.n_blocks * S; i += blockDim.x) sw4[i] = gw[i];
-    __syncthreads();
-  }
-  constexpr int D = (MODE == 3) ? ORDER + 1 : 1;
-  constexpr int NT = (MODE == 3) ? (ORDER == 2 ? 6 : 10) : 1;   // pairs a + b <= ORDER
-  constexpr int NM = (MODE == 3) ? (ORDER == 2 ? 10 : 20) : 1;  // triples a + b + c <= ORDER
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int64_t total = n_faces * op.max_items;
-  for (int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; item < total; item += nwarps) {
-    const int64_t f = item / op.max_items;
-    const int it = int(item - f * op.max_items);
-    const th_face* fp = faces + f;
-    FaceRef fr;
-    decode_face(fp, op, fr);
-    int g0, g1, g2;
-    if (!decode_item(op, fr, it, g0, g1, g2)) continue;
-    const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]), G2 = __ldg(&op.grp1[g2]);
-    const int bid = (MODE == 1) ? __ldg(&op.block_id[(g0 * op.G1 + g1) * op.G1 + g2]) : 0;
-    // per-item uniform tables
-    double R0[C0][L0], R1[CT][LT], R2[CT][LT];
-    if constexpr (MODE == 2) {
-      const double* r0 = op.rows0 + __ldg(&op.row_off0[g0]);
-      const double* r1 = op.rows1 + __ldg(&op.row_off1[g1]);
-      const double* r2 = op.rows1 + __ldg(&op.row_off1[g2]);
-#pragma unroll
-      for (int c = 0; c < C0; ++c)
-#pragma unroll
-        for (int x = 0; x < L0; ++x) R0[c][x] = c < G0.w ? __ldg(r0 + c * L0 + x) : 0.0;
-#pragma unroll
-      for (int c = 0; c < CT; ++c)
-#pragma unroll
-        for (int x = 0; x < LT; ++x) {
-          R1[c][x] = c < G1.w ? __ldg(r1 + c * LT + x) : 0.0;
-          R2[c][x] = c < G2.w ? __ldg(r2 + c * LT + x) : 0.0;
-        }
-    }
-    const double* __restrict__ Wg = op.weights + (MODE == 1 ? __ldg(&op.block_off[bid]) : 0);
-    const double4* __restrict__ Ws = sw4 + (SMEM_W ? bid * S : 0);
-    for (int cb = 0; cb < u; cb += 32 * NU) {
-      bool ok[NU];
-#pragma unroll
-      for (int q = 0; q < NU; ++q) ok[q] = cb + lane + 32 * q < u;
-      double acc[MODE == 3 ? NM : CH][NU];
-#pragma unroll
-      for (int c = 0; c < (MODE == 3 ? NM : CH); ++c)
-#pragma unroll
-        for (int q = 0; q < NU; ++q) acc[c][q] = 0.0;
-#pragma unroll(LT == 3 ? LT : 1)
-      for (int z = 0; z < LT; ++z) {
-        double T[MODE == 3 ? NT : C0 * CT][NU];
-#pragma unroll
-        for (int c = 0; c < (MODE == 3 ? NT : C0 * CT); ++c)
-#pragma unroll
-          for (int q = 0; q < NU; ++q) T[c][q] = 0.0;
-        double v[LT][L0][NU];
-#pragma unroll
-        for (int y = 0; y < LT; ++y) {
-          const double* row = src + src_addr(fp, op, fr, G0.x, G1.x + y, G2.x + z) + cb + lane;
-#pragma unroll
-          for (int x = 0; x < L0; ++x)
-#pragma unroll
-            for (int q = 0; q < NU; ++q) v[y][x][q] = ok[q] ? __ldg(row + int64_t(x) * fr.sn + 32 * q) : 0.0;
-        }
-#pragma unroll
-        for (int y = 0; y < LT; ++y) {
-          if constexpr (MODE == 1) {
-#pragma unroll
-            for (int x = 0; x < L0; ++x) {
-              const int cell = x + L0 * (y + LT * z);
-              if constexpr (SMEM_W) {
-                const double4 w = Ws[cell];
-                const double wc[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int c = 0; c < CH; ++c)
-#pragma unroll
-                  for (int q = 0; q < NU; ++q) acc[c][q] = fma(wc[c], v[y][x][q], acc[c][q]);
-              } else {
-                const double2* wr = reinterpret_cast<const double2*>(Wg + int64_t(cell) * ((CH + 1) & ~1));
-#pragma unroll
-                for (int c = 0; c < CH; c += 2) {
-                  const double2 w = __ldg(wr + c / 2);
-#pragma unroll
-                  for (int q = 0; q < NU; ++q) {
-                    acc[c][q] = fma(w.x, v[y][x][q], acc[c][q]);
-                    if (c + 1 < CH) acc[c + 1][q] = fma(w.y, v[y][x][q], acc[c + 1][q]);
-                  }
-                }
-              }
-            }
-          } else if constexpr (MODE == 2) {
-#pragma unroll
-            for (int c0 = 0; c0 < C0; ++c0) {
-#pragma unroll
-              for (int q = 0; q < NU; ++q) {
-                double tx = 0.0;
-#pragma unroll
-                for (int x = 0; x < L0; ++x) tx = fma(R0[c0][x], v[y][x][q], tx);
-#pragma unroll
-                for (int c1 = 0; c1 < CT; ++c1) T[c0 + C0 * c1][q] = fma(R1[c1][y], tx, T[c0 + C0 * c1][q]);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < NU; ++q) {
-              double m[D];
-#pragma unroll
-              for (int a = 0; a < D; ++a) {
-                m[a] = 0.0;
-#pragma unroll
-                for (int x = 0; x < L0; ++x) {
-                  const double g = Gram<L0>::P(a, x);
-                  if (g == 1.0) m[a] += v[y][x][q];
-                  else if (g == -1.0) m[a] -= v[y][x][q];
-                  else if (g != 0.0) m[a] = fma(g, v[y][x][q], m[a]);
-                }
-              }
-              int t = 0;
-#pragma unroll
-              for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int b = 0; b + a < D; ++b, ++t) {
-                  const double g = Gram<LT>::P(b, y);
-                  if (g == 1.0) T[t][q] += m[a];
-                  else if (g == -1.0) T[t][q] -= m[a];
-                  else if (g != 0.0) T[t][q] = fma(g, m[a], T[t][q]);
-                }
-            }
-          }
-        }
-        if constexpr (MODE == 2) {
-#pragma unroll
-          for (int c2 = 0; c2 < CT; ++c2)
-#pragma unroll
-            for (int c01 = 0; c01 < C0 * CT; ++c01)
-#pragma unroll
-              for (int q = 0; q < NU; ++q) acc[c01 + C0 * CT * c2][q] = fma(R2[c2][z], T[c01][q], acc[c01 + C0 * CT * c2][q]);
-        } else if constexpr (MODE == 3) {
-          double pz[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) pz[c] = gram_rt<LT>(c, z);
-          int t = 0, mi = 0;
-#pragma unroll
-          for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int b = 0; b + a < D; ++b, ++t)
-#pragma unroll
-              for (int c = 0; c + b + a < D; ++c, ++mi)
-#pragma unroll
-                for (int q = 0; q < NU; ++q) acc[mi][q] = fma(pz[c], T[t][q], acc[mi][q]);
-        }
-      }
-      // ---- store -----------------------------------------------------------
-      bool bad = false;
-      auto put = [&](int i0, int i1, int i2, int q, double val) {
-        const int t0 = G0.z + i0, t1 = G1.z + i1, t2 = G2.z + i2;
-        if (i0 < G0.w && i1 < G1.w && i2 < G2.w && t0 >= fr.lo0 && t0 < fr.hi0 && t1 >= fr.lo1 &&
-            t1 < fr.lo1 + op.p && t2 >= fr.lo2 && t2 < fr.lo2 + op.p && ok[q]) {
-          dst[fr.dst + (t0 - fr.lo0) * fr.dn + (t1 - fr.lo1) * fr.d1 + (t2 - fr.lo2) * fr.d2 + cb + lane + 32 * q] = val;
-          bad |= !isfinite(val);
-        }
-      };
-      if constexpr (MODE == 3) {
-        const double* s0 = op.synth0 + g0 * 12;
-        const double* s1 = op.synth1 + g1 * 12;
-        const double* s2 = op.synth1 + g2 * 12;
-#pragma unroll
-        for (int l = 0; l < CT; ++l) {
-          double S2v[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) S2v[c] = __ldg(s2 + l * 4 + c);
-#pragma unroll
-          for (int q = 0; q < NU; ++q) {
-            double Q[NT];
-            int t = 0, mi = 0;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-              for (int b = 0; b + a < D; ++b, ++t) {
-                double s = 0.0;
-#pragma unroll
-                for (int c = 0; c + b + a < D; ++c, ++mi) s = fma(S2v[c], acc[mi][q], s);
-                Q[t] = s;
-              }
-#pragma unroll
-            for (int j = 0; j < CT; ++j) {
-              double Rv[D];
-              int tt = 0;
-#pragma unroll
-              for (int a = 0; a < D; ++a) {
-                double s = 0.0;
-#pragma unroll
-                for (int b = 0; b + a < D; ++b, ++tt) s = fma(__ldg(s1 + j * 4 + b), Q[tt], s);
-                Rv[a] = s;
-              }
-#pragma unroll
-              for (int i = 0; i < C0; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int a = 0; a < D; ++a) s = fma(__ldg(s0 + i * 4 + a), Rv[a], s);
-                put(i, j, l, q, s);
-              }
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          const int i0 = c % C0, i1 = (c / C0) % CT, i2 = c / (C0 * CT);
-#pragma unroll
-          for (int q = 0; q < NU; ++q) put(i0, i1, i2, q, acc[c][q]);
-        }
-      }
-      raise_flag(flag, bad);
-    }
-  }
-}
+#include "window.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -719,6 +450,10 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   op->max_children *= mc1 * mc1;
   op->on_device = upload_to_device;
   d.n_blocks = (int32_t)h.block_off.size();
+  d.units_per_face = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b)
+      d.units_per_face = std::max(d.units_per_face, (h.half_g[a][1] - h.half_g[a][0]) * (h.seg_g[b][1] - h.seg_g[b][0]));
   op->smem_ok = h.fast_mode == 1 && h.fast_C0 * h.fast_CT * h.fast_CT <= 4;
   for (size_t b = 0; b < h.block_cp.size() && op->smem_ok; ++b)
     op->smem_ok = h.block_cp[b] == 4 &&
@@ -807,7 +542,9 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   do {                                                                                                 \
     auto kfn = window_kernel<MODE, L, L, 3, CT, ORDER, NU>;                                          \
     if (SMEM > 48 * 1024) TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM))); \
-    kfn<<<blocks, threads, SMEM, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                    \
+    const int64_t units = n_faces * int64_t(op->dev.units_per_face);                                  \
+    const int wblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 16));              \
+    kfn<<<wblocks, threads, SMEM, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                    \
   } while (0)
   if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
   else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0);
