@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 }
 
 #include "window.cuh"
+#include "restrict_pipe.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -546,7 +547,22 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int wblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 16));              \
     kfn<<<wblocks, threads, SMEM, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                    \
   } while (0)
-  if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
+#define TH_PIPE(MODE, L, NST, WARPS, CTAS)                                                             \
+  do {                                                                                                 \
+    auto kfn = restrict_pipe_kernel<MODE, L, L, NST, WARPS>;                                           \
+    const size_t smem = (MODE == 1 ? op->smem_bytes : 0) + size_t(WARPS) * NST * L * L * 64 * 8;       \
+    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));       \
+    const int64_t warps_needed = n_faces * int64_t(op->dev.max_items);                                \
+    const int pblocks = int(std::min<int64_t>((warps_needed + WARPS - 1) / WARPS, int64_t(num_sms()) * CTAS)); \
+    kfn<<<pblocks, WARPS * 32, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                 \
+  } while (0)
+  const bool pipe_ok = !interp && h.fast_C0 == 3 && h.fast_CT == 1 &&
+                       ((h.fast_mode == 1 && op->smem_ok) || h.fast_mode == 2);
+  if (pipe_ok && h.fast_mode == 1 && h.fast_L0 == 3) TH_PIPE(1, 3, 6, 4, 2);
+  else if (pipe_ok && h.fast_mode == 1 && h.fast_L0 == 5) TH_PIPE(1, 5, 3, 4, 1);
+  else if (pipe_ok && h.fast_mode == 2 && h.fast_L0 == 3) TH_PIPE(2, 3, 6, 4, 2);
+#undef TH_PIPE
+  else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
   else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0);
   else if (h.fast_mode == 2 && h.fast_L0 == 3 && interp) TH_WIN(2, 3, 3, 0, 1, 0);
   else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 2, 0);
