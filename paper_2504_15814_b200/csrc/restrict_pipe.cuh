@@ -1,244 +1,138 @@
-// Pipelined restriction (included by trihalo.cu).
+// Restriction kernel (included by trihalo.cu): the HBM-bound hot loop.
 //
 // Restriction streams ~9x more fine-source bytes than it writes (SURVEY
-// §8a A1, 1.15 MB per p=9 face), so the kernel is organised around keeping
-// HBM busy: each warp walks a contiguous range of (face, column) work items
-// and runs an NST-deep ring of shared-memory slices filled with cp.async
-// (8-byte LDGSTS: the unpadded u = 59 AoS cells are only 8-byte aligned, which
-// rules out TMA bulk copies).  A slice is one z-plane of a block's window
-// (LT x L0 cells x up to 64 unknowns); slice s+NST-1 is issued before slice s
-// is consumed, so NST-1 slices per warp are in flight without holding
-// registers.  Address work is hoisted: faces are decoded only when the face
-// changes (the nine fine-block bases go to a per-warp shared cache), per-face
-// normal offsets and per-item row offsets are precomputed, so one cp.async
-// pair costs one 64-bit add.  Dense weights (<= 4 children) sit in shared
-// memory and are read as broadcasts; 2 unknowns per lane.
-//   MODE 1  dense  out[c] = sum_cell W[cell][c] v[cell]          (order2/3, matrix_linear)
+// §8a A1: 1.15 MB per p = 9 face for order2, 1.84 MB for order3).  Measured
+// on B200 (profiles/r01_probe_load_paths.txt), the fastest way to stream the
+// unpadded u = 59 AoS cells (472 B, 8-byte aligned) is plain LDG.64 into
+// registers at >= 24-32 resident warps per SM; 8-byte cp.async tops out near
+// 5.5 TB/s and TMA needs 16-byte aligned cells.  So this kernel is built for
+// occupancy: one unknown per lane (u in chunks of 32), the window streamed one
+// z-slice (L x L cells) at a time, and the weights in the constant bank as a
+// __grid_constant__ kernel parameter (DFMA reads them as c[][] operands: no
+// shared-memory traffic, no registers).
+//   MODE 1  dense  out[c] = sum_cell W[cls][cell][c] v[cell]     (order2/3, matrix_linear)
 //   MODE 2  tensor normal, then t1, then t2 1-D rows              (tensor_linear, linear.py:115-151)
+// Requirements (checked on the host): k = 3 restriction with one normal group
+// of 3 children and window L, every tangential group 1 child with window L,
+// <= NCLS distinct dense blocks; for MODE 2 all tangential rows equal.
 #pragma once
 
-__device__ __forceinline__ void cp_async8(unsigned smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_dst), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+// read-only global load the compiler may not move across the per-slice
+// barrier below (a plain __ldg is treated as a constant read and hoisted,
+// which multiplies the live registers by the window depth and spills)
+__device__ __forceinline__ double ldg_slice(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
 }
 
-template <int MODE, int L0, int LT, int NST, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) restrict_pipe_kernel(DevOp op, const double* __restrict__ src,
-                                                                   double* __restrict__ dst,
-                                                                   const th_face* __restrict__ faces,
-                                                                   int64_t n_faces, int u, int32_t* flag) {
-  constexpr int SL = L0 * LT;      // cells per slice
-  constexpr int S = L0 * LT * LT;  // cells per window
-  constexpr int C0 = 3;            // normal children (k = 3); t1 / t2 children 1
-  constexpr int SLOT = SL * 64;    // doubles per ring slot
-  extern __shared__ double4 smem4[];
-  __shared__ int64_t face_base[WARPS][9];
-  double4* sw4 = smem4;  // dense weights [blk][cell] (MODE 1)
-  const int n_w4 = MODE == 1 ? op.n_blocks * S : 0;
-  double* ring = reinterpret_cast<double*>(smem4 + n_w4);
+template <int MODE, int L, int NCLS>
+struct RestrictParams {
+  double w[MODE == 1 ? NCLS : 1][MODE == 1 ? L * L * L : 1][3];  // dense blocks [cls][cell][child]
+  double r0[3][L];                                               // tensor rows: normal
+  double rt[L];                                                  //              tangential
+};
+
+template <int MODE, int L, int NCLS, int MINB>
+__global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
+                                                                 const __grid_constant__ RestrictParams<MODE, L, NCLS> P,
+                                                                 const double* __restrict__ src,
+                                                                 double* __restrict__ dst,
+                                                                 const th_face* __restrict__ faces, int64_t n_faces,
+                                                                 int u, int32_t* flag) {
+  // dense weights are staged once per CTA in shared memory and read as
+  // broadcast LDS with compile-time offsets: left in the constant bank, the
+  // compiler hoists all of them into (uniform) registers and spills
+  __shared__ double sw[MODE == 1 ? NCLS * L * L * L * 3 : 1];
   if constexpr (MODE == 1) {
-    const double4* gw = reinterpret_cast<const double4*>(op.weights);
-    for (int i = threadIdx.x; i < n_w4; i += blockDim.x) sw4[i] = gw[i];
+    const double* pw = &P.w[0][0][0];
+    for (int i = threadIdx.x; i < NCLS * L * L * L * 3; i += blockDim.x) sw[i] = pw[i];
+    __syncthreads();
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  double* my_ring = ring + size_t(warp) * NST * SLOT;
-  const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(my_ring)) + lane * 8u;
-  const int64_t total = n_faces * op.max_items;
-  const int64_t nw = int64_t(gridDim.x) * WARPS;
-  const int64_t gid = int64_t(blockIdx.x) * WARPS + warp;
-  const int64_t per = (total + nw - 1) / nw;
-  const int64_t i_begin = min(total, gid * per), i_end = min(total, i_begin + per);
-  const int n_chunks = (u + 63) / 64;
-  const int64_t n_slices = (i_end - i_begin) * n_chunks * LT;
   const int p = op.p;
-
-  // ---- issuer state --------------------------------------------------------
-  int64_t i_face = -1, i_item = -1;
-  FaceRef ifr;
-  int64_t ixo[L0], iyo[LT];
-  int iyb[LT];
-  int4 iG2;
-  bool i_valid = false;
-  // ---- consumer state ------------------------------------------------------
-  int64_t c_face = -1, c_item = -1;
-  FaceRef cfr;
-  int4 cG0, cG1, cG2;
-  int cg0 = 0, cg1 = 0, cg2 = 0;
-  bool c_valid = false;
-
-  auto issue = [&](int64_t s) {
-    if (s < n_slices) {
-      const int64_t ic = s / LT;
-      const int z = int(s - ic * LT);
-      const int64_t item = i_begin + ic / n_chunks;
-      const int cb = int(ic - (ic / n_chunks) * n_chunks) * 64;
-      if (item != i_item) {
-        i_item = item;
-        const int64_t f = item / op.max_items;
-        if (f != i_face) {
-          i_face = f;
-          decode_face(faces + f, op, ifr);
-          const int64_t adj = ifr.src0 - __ldg(&faces[f].src[0]);
-          __syncwarp();
-          if (lane < 9) face_base[warp][lane] = __ldg(&faces[f].src[lane]) + adj;
-          __syncwarp();
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = n_faces * op.max_items;
+  for (int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; item < total; item += nwarps) {
+    const int64_t f = item / op.max_items;
+    const th_face* fp = faces + f;
+    FaceRef fr;
+    decode_face(fp, op, fr);
+    int g0, g1, g2;
+    if (!decode_item(op, fr, int(item - f * op.max_items), g0, g1, g2)) continue;
+    const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]), G2 = __ldg(&op.grp1[g2]);
+    const int cls = (MODE == 1 && NCLS > 1) ? __ldg(&op.block_id[(g0 * op.G1 + g1) * op.G1 + g2]) : 0;
+    const int64_t adj = fr.src0 - __ldg(&fp->src[0]) + int64_t(G0.x) * fr.sn + lane;
+    // per-row (t1) offsets and fine-block column
+    int64_t yo[L];
+    int yb[L];
 #pragma unroll
-          for (int x = 0; x < L0; ++x) ixo[x] = int64_t(x) * ifr.sn;
-        }
-        int g0, g1, g2;
-        i_valid = decode_item(op, ifr, int(item - f * op.max_items), g0, g1, g2);
-        if (i_valid) {
-          const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]);
-          iG2 = __ldg(&op.grp1[g2]);
+    for (int y = 0; y < L; ++y) {
+      const int a1 = G1.x + y;
+      yb[y] = (a1 >= p) + (a1 >= 2 * p);
+      yo[y] = int64_t(a1 - yb[y] * p) * fr.s1;
+    }
+    const int t1 = G1.z, t2 = G2.z;
+    const bool in_box = t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p;
+    const int64_t obase = fr.dst + (t1 - fr.lo1) * fr.d1 + (t2 - fr.lo2) * fr.d2 + lane;
+    for (int cb = 0; cb < u; cb += 32) {
+      const bool ok = cb + lane < u;
+      double acc[3] = {0.0, 0.0, 0.0};
+      constexpr int ZU = (L == 3) ? L : 1;  // 3x3x3 windows unroll fully, 5x5x5 stream slice by slice
+#pragma unroll 1
+      for (int z0 = 0; z0 < L; z0 += ZU)
 #pragma unroll
-          for (int y = 0; y < LT; ++y) {
-            const int a1 = G1.x + y;
-            iyb[y] = (a1 >= p) + (a1 >= 2 * p);
-            iyo[y] = int64_t(a1 - iyb[y] * p) * ifr.s1 + int64_t(G0.x) * ifr.sn;
-          }
-        }
-      }
-      if (i_valid) {
-        const int a2 = iG2.x + z;
+      for (int dz = 0; dz < ZU; ++dz) {
+        const int z = z0 + dz;
+        const int a2 = G2.x + z;
         const int b2 = (a2 >= p) + (a2 >= 2 * p);
-        const int64_t zo = int64_t(a2 - b2 * p) * ifr.s2 + cb + lane;
-        const unsigned slot = ring_s + unsigned((s % NST) * SLOT) * 8u;
-        const bool ok0 = cb + lane < u, ok1 = cb + lane + 32 < u;
+        const int64_t zo = int64_t(a2 - b2 * p) * fr.s2 + adj + cb;
+        double v[L][L];
 #pragma unroll
-        for (int y = 0; y < LT; ++y) {
-          const double* row = src + (face_base[warp][iyb[y] + 3 * b2] + iyo[y] + zo);
+        for (int y = 0; y < L; ++y) {
+          const double* row = src + (__ldg(&fp->src[yb[y] + 3 * b2]) + yo[y] + zo);
 #pragma unroll
-          for (int x = 0; x < L0; ++x) {
-            const double* g = row + ixo[x];
-            const unsigned d = slot + unsigned((y * L0 + x) * 64 * 8);
-            if (ok0) cp_async8(d, g);
-            if (ok1) cp_async8(d + 256u, g + 32);
-          }
+          for (int x = 0; x < L; ++x) v[y][x] = ok ? ldg_slice(row + int64_t(x) * fr.sn) : 0.0;
         }
-      }
-    }
-    cp_async_commit();
-  };
-
-#pragma unroll
-  for (int s = 0; s < NST - 1; ++s) issue(s);
-
-  double acc[C0][2];
-  double R0[MODE == 2 ? C0 : 1][MODE == 2 ? L0 : 1], R1[MODE == 2 ? LT : 1], R2[MODE == 2 ? LT : 1];
-  const double4* Ws = sw4;
-  int64_t obase = 0;
-  bool store_ok = false;
-  for (int64_t s = 0; s < n_slices; ++s) {
-    issue(s + NST - 1);
-    const int64_t ic = s / LT;
-    const int z = int(s - ic * LT);
-    const int64_t item = i_begin + ic / n_chunks;
-    const int cb = int(ic - (ic / n_chunks) * n_chunks) * 64;
-    if (item != c_item) {
-      c_item = item;
-      const int64_t f = item / op.max_items;
-      if (f != c_face) {
-        c_face = f;
-        decode_face(faces + f, op, cfr);
-      }
-      c_valid = decode_item(op, cfr, int(item - f * op.max_items), cg0, cg1, cg2);
-      if (c_valid) {
-        cG0 = __ldg(&op.grp0[cg0]);
-        cG1 = __ldg(&op.grp1[cg1]);
-        cG2 = __ldg(&op.grp1[cg2]);
         if constexpr (MODE == 1) {
-          Ws = sw4 + __ldg(&op.block_id[(cg0 * op.G1 + cg1) * op.G1 + cg2]) * S;
+#pragma unroll
+          for (int y = 0; y < L; ++y)
+#pragma unroll
+            for (int x = 0; x < L; ++x) {
+              const int cell = x + L * (y + L * z);
+#pragma unroll
+              for (int c = 0; c < 3; ++c) acc[c] = fma(sw[(cls * L * L * L + cell) * 3 + c], v[y][x], acc[c]);
+            }
         } else {
-          const double* r0 = op.rows0 + __ldg(&op.row_off0[cg0]);
-          const double* r1 = op.rows1 + __ldg(&op.row_off1[cg1]);
-          const double* r2 = op.rows1 + __ldg(&op.row_off1[cg2]);
+          double T[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-          for (int c = 0; c < C0; ++c)
+          for (int y = 0; y < L; ++y)
 #pragma unroll
-            for (int x = 0; x < L0; ++x) R0[c][x] = c < cG0.w ? __ldg(r0 + c * L0 + x) : 0.0;
+            for (int c = 0; c < 3; ++c) {
+              double t = 0.0;
 #pragma unroll
-          for (int y = 0; y < LT; ++y) {
-            R1[y] = __ldg(r1 + y);
-            R2[y] = __ldg(r2 + y);
-          }
-        }
-        const int t1 = cG1.z, t2 = cG2.z;
-        store_ok = t1 >= cfr.lo1 && t1 < cfr.lo1 + p && t2 >= cfr.lo2 && t2 < cfr.lo2 + p;
-        obase = cfr.dst + (t1 - cfr.lo1) * cfr.d1 + (t2 - cfr.lo2) * cfr.d2 + lane;
-      }
-    }
-    cp_async_wait<NST - 1>();
-    __syncwarp();
-    if (c_valid) {
-      if (z == 0) {
-#pragma unroll
-        for (int c = 0; c < C0; ++c) acc[c][0] = acc[c][1] = 0.0;
-      }
-      const double* slot = my_ring + size_t(s % NST) * SLOT + lane;
-      if constexpr (MODE == 1) {
-        const double4* W = Ws + z * SL;
-#pragma unroll
-        for (int c = 0; c < SL; ++c) {
-          const double v0 = slot[c * 64], v1 = slot[c * 64 + 32];
-          const double4 w = W[c];
-          acc[0][0] = fma(w.x, v0, acc[0][0]);
-          acc[0][1] = fma(w.x, v1, acc[0][1]);
-          acc[1][0] = fma(w.y, v0, acc[1][0]);
-          acc[1][1] = fma(w.y, v1, acc[1][1]);
-          acc[2][0] = fma(w.z, v0, acc[2][0]);
-          acc[2][1] = fma(w.z, v1, acc[2][1]);
-        }
-      } else {
-        double T[C0][2];
-#pragma unroll
-        for (int c = 0; c < C0; ++c) T[c][0] = T[c][1] = 0.0;
-#pragma unroll
-        for (int y = 0; y < LT; ++y)
-#pragma unroll
-          for (int c = 0; c < C0; ++c) {
-            double t0 = 0.0, t1 = 0.0;
-#pragma unroll
-            for (int x = 0; x < L0; ++x) {
-              t0 = fma(R0[c][x], slot[(y * L0 + x) * 64], t0);
-              t1 = fma(R0[c][x], slot[(y * L0 + x) * 64 + 32], t1);
+              for (int x = 0; x < L; ++x) t = fma(P.r0[c][x], v[y][x], t);
+              T[c] = fma(P.rt[y], t, T[c]);
             }
-            T[c][0] = fma(R1[y], t0, T[c][0]);
-            T[c][1] = fma(R1[y], t1, T[c][1]);
-          }
-        double r2 = R2[0];
 #pragma unroll
-        for (int zz = 1; zz < LT; ++zz)
-          if (zz == z) r2 = R2[zz];
-#pragma unroll
-        for (int c = 0; c < C0; ++c) {
-          acc[c][0] = fma(r2, T[c][0], acc[c][0]);
-          acc[c][1] = fma(r2, T[c][1], acc[c][1]);
+          for (int c = 0; c < 3; ++c) acc[c] = fma(P.rt[z], T[c], acc[c]);
         }
+        // keep the next slice's loads below this slice's math: registers stay
+        // at one slice (occupancy, not per-warp depth, hides the latency)
+        asm volatile("" ::: "memory");
       }
-      if (z == LT - 1) {  // window complete: store the children inside the face's box
-        bool bad = false;
-        if (store_ok) {
-          const bool ok0 = cb + lane < u, ok1 = cb + lane + 32 < u;
+      bool bad = false;
+      if (in_box && ok) {
 #pragma unroll
-          for (int c = 0; c < C0; ++c) {
-            const int t0 = cG0.z + c;
-            if (c < cG0.w && t0 >= cfr.lo0 && t0 < cfr.hi0) {
-              double* dp = dst + obase + cb + (t0 - cfr.lo0) * cfr.dn;
-              if (ok0) { dp[0] = acc[c][0]; bad |= !isfinite(acc[c][0]); }
-              if (ok1) { dp[32] = acc[c][1]; bad |= !isfinite(acc[c][1]); }
-            }
+        for (int c = 0; c < 3; ++c) {
+          const int t0 = G0.z + c;
+          if (c < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) {
+            dst[obase + cb + (t0 - fr.lo0) * fr.dn] = acc[c];
+            bad |= !isfinite(acc[c]);
           }
         }
-        raise_flag(flag, bad);
       }
+      raise_flag(flag, bad);
     }
-    __syncwarp();
   }
-  cp_async_wait<0>();
 }

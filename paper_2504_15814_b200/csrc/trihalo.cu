@@ -365,9 +365,60 @@ struct th_operator {
   bool on_device = false;
   bool smem_ok = false;
   size_t smem_bytes = 0;
+  // restriction register kernel: mode (0 = not eligible), window, classes, params blob
+  int r_mode = 0, r_L = 0, r_ncls = 0;
+  std::vector<unsigned char> r_params;
 };
 
 namespace {
+
+template <int MODE, int L, int NCLS>
+bool fill_restrict_params(const th::HostOperator& h, std::vector<unsigned char>& blob) {
+  using PT = RestrictParams<MODE, L, NCLS>;
+  PT prm;
+  std::memset(&prm, 0, sizeof(prm));
+  constexpr int S = L * L * L;
+  if (MODE == 1) {
+    if ((int)h.block_off.size() > NCLS) return false;
+    for (size_t b = 0; b < h.block_off.size(); ++b) {
+      if (h.block_cp[b] != 4) return false;
+      for (int cell = 0; cell < S; ++cell)
+        for (int c = 0; c < 3; ++c) prm.w[b][cell][c] = h.weights[h.block_off[b] + size_t(cell) * 4 + c];
+    }
+  } else {
+    if (h.groups[0].size() != 1 || h.rows[0].size() != size_t(3 * L)) return false;
+    for (int c = 0; c < 3; ++c)
+      for (int x = 0; x < L; ++x) prm.r0[c][x] = h.rows[0][c * L + x];
+    for (size_t g = 0; g < h.groups[1].size(); ++g)
+      for (int y = 0; y < L; ++y) {
+        const double v = h.rows[1][h.row_off[1][g] + y];
+        if (g == 0) prm.rt[y] = v;
+        else if (v != prm.rt[y]) return false;
+      }
+  }
+  blob.resize(sizeof(PT));
+  std::memcpy(blob.data(), &prm, sizeof(PT));
+  return true;
+}
+
+// eligibility of the register restriction kernel (restrict_pipe.cuh)
+void prepare_restrict(th_operator* op) {
+  const th::HostOperator& h = op->host;
+  op->r_mode = 0;
+  if (h.role != 1 || h.k != 3 || h.fast_C0 != 3 || h.fast_CT != 1 || h.groups[0].size() != 1 ||
+      h.groups[0][0].tgtN != 3)
+    return;
+  for (const auto& g : h.groups[1])
+    if (g.tgtN != 1) return;
+  bool ok = false;
+  if (h.fast_mode == 1 && h.fast_L0 == 3) ok = fill_restrict_params<1, 3, 1>(h, op->r_params), op->r_ncls = 1;
+  else if (h.fast_mode == 1 && h.fast_L0 == 5) ok = fill_restrict_params<1, 5, 9>(h, op->r_params), op->r_ncls = 9;
+  else if (h.fast_mode == 2 && h.fast_L0 == 3) ok = fill_restrict_params<2, 3, 1>(h, op->r_params), op->r_ncls = 1;
+  if (ok) {
+    op->r_mode = h.fast_mode;
+    op->r_L = h.fast_L0;
+  }
+}
 
 template <class T>
 int32_t upload(th_operator* op, const std::vector<T>& v, const T** out) {
@@ -461,6 +512,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
                   h.block_off[b] == int64_t(b) * 4 * h.fast_L0 * h.fast_LT * h.fast_LT;
   op->smem_bytes = op->smem_ok ? size_t(d.n_blocks) * h.fast_L0 * h.fast_LT * h.fast_LT * 32 : 0;
   if (op->smem_bytes > 200 * 1024) op->smem_ok = false;
+  prepare_restrict(op);
   if (!upload_to_device) {
     *out = op;
     return TH_OK;
@@ -547,21 +599,18 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int wblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 16));              \
     kfn<<<wblocks, threads, SMEM, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                    \
   } while (0)
-#define TH_PIPE(MODE, L, NST, WARPS, CTAS)                                                             \
+#define TH_RREG(MODE, L, NCLS, MINB, CTAS)                                                            \
   do {                                                                                                 \
-    auto kfn = restrict_pipe_kernel<MODE, L, L, NST, WARPS>;                                           \
-    const size_t smem = (MODE == 1 ? op->smem_bytes : 0) + size_t(WARPS) * NST * L * L * 64 * 8;       \
-    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));       \
+    using PT = RestrictParams<MODE, L, NCLS>;                                                          \
+    const PT* prm = reinterpret_cast<const PT*>(op->r_params.data());                                 \
     const int64_t warps_needed = n_faces * int64_t(op->dev.max_items);                                \
-    const int pblocks = int(std::min<int64_t>((warps_needed + WARPS - 1) / WARPS, int64_t(num_sms()) * CTAS)); \
-    kfn<<<pblocks, WARPS * 32, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                 \
+    const int rblocks = int(std::min<int64_t>((warps_needed + 3) / 4, int64_t(num_sms()) * CTAS));    \
+    restrict_reg_kernel<MODE, L, NCLS, MINB><<<rblocks, 128, 0, s>>>(op->dev, *prm, src, dst, faces, n_faces, u, flag); \
   } while (0)
-  const bool pipe_ok = !interp && h.fast_C0 == 3 && h.fast_CT == 1 &&
-                       ((h.fast_mode == 1 && op->smem_ok) || h.fast_mode == 2);
-  if (pipe_ok && h.fast_mode == 1 && h.fast_L0 == 3) TH_PIPE(1, 3, 6, 4, 2);
-  else if (pipe_ok && h.fast_mode == 1 && h.fast_L0 == 5) TH_PIPE(1, 5, 3, 4, 1);
-  else if (pipe_ok && h.fast_mode == 2 && h.fast_L0 == 3) TH_PIPE(2, 3, 6, 4, 2);
-#undef TH_PIPE
+  if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 6, 12);
+  else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 5, 10);
+  else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 6, 12);
+#undef TH_RREG
   else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
   else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0);
   else if (h.fast_mode == 2 && h.fast_L0 == 3 && interp) TH_WIN(2, 3, 3, 0, 1, 0);
