@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -599,17 +600,22 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int wblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 16));              \
     kfn<<<wblocks, threads, SMEM, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                    \
   } while (0)
-#define TH_RREG(MODE, L, NCLS, MINB, CTAS)                                                            \
+#define TH_RREG(MODE, L, NCLS, NU, MINB, CTAS)                                                        \
   do {                                                                                                 \
     using PT = RestrictParams<MODE, L, NCLS>;                                                          \
     const PT* prm = reinterpret_cast<const PT*>(op->r_params.data());                                 \
     const int64_t warps_needed = n_faces * int64_t(op->dev.max_items);                                \
     const int rblocks = int(std::min<int64_t>((warps_needed + 3) / 4, int64_t(num_sms()) * CTAS));    \
-    restrict_reg_kernel<MODE, L, NCLS, MINB><<<rblocks, 128, 0, s>>>(op->dev, *prm, src, dst, faces, n_faces, u, flag); \
+    restrict_reg_kernel<MODE, L, NCLS, NU, MINB><<<rblocks, 128, 0, s>>>(op->dev, *prm, src, dst, faces, n_faces, u, flag); \
   } while (0)
-  if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 6, 12);
-  else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 5, 10);
-  else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 6, 12);
+  // TH_RESTRICT_NU=1 selects the one-unknown-per-lane variant (tuning experiments)
+  static const int rnu = [] { const char* e = std::getenv("TH_RESTRICT_NU"); return e && e[0] == '1' ? 1 : 2; }();
+  if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
+  else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 1, 6, 12);
+  else if (op->r_mode == 1 && op->r_L == 5 && rnu == 2) TH_RREG(1, 5, 9, 2, 4, 8);
+  else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 1, 5, 10);
+  else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2) TH_RREG(2, 3, 1, 2, 5, 10);
+  else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 1, 6, 12);
 #undef TH_RREG
   else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
   else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0);
