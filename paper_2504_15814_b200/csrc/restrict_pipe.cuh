@@ -26,6 +26,15 @@ __device__ __forceinline__ double ldg_slice(const double* p) {
   return v;
 }
 
+// TMA bulk prefetch of one AoS cell (u doubles) into L2; the range is widened
+// to 16-byte alignment as cp.async.bulk.prefetch requires
+__device__ __forceinline__ void l2_prefetch_cell(const double* cell, int u) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(cell);
+  const uintptr_t lo = a & ~uintptr_t(15);
+  const unsigned bytes = unsigned((a + uintptr_t(u) * 8 - lo + 15) & ~uintptr_t(15));
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(bytes) : "memory");
+}
+
 template <int MODE, int L, int NCLS>
 struct RestrictParams {
   double w[MODE == 1 ? NCLS : 1][MODE == 1 ? L * L * L : 1][3];  // dense blocks [cls][cell][child]
@@ -72,6 +81,16 @@ __global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
       const int a1 = G1.x + y;
       yb[y] = (a1 >= p) + (a1 >= 2 * p);
       yo[y] = int64_t(a1 - yb[y] * p) * fr.s1;
+    }
+    // L2 bulk prefetch of the whole window (one cell per lane): the slices
+    // below then stream from L2 while only one slice is held in registers
+    for (int cell = lane; cell < L * L * L; cell += 32) {
+      const int x = cell % L, y = (cell / L) % L, z = cell / (L * L);
+      const int a1 = G1.x + y, a2 = G2.x + z;
+      const int b1 = (a1 >= p) + (a1 >= 2 * p), b2 = (a2 >= p) + (a2 >= 2 * p);
+      const int64_t e = __ldg(&fp->src[b1 + 3 * b2]) + int64_t(a1 - b1 * p) * fr.s1 +
+                        int64_t(a2 - b2 * p) * fr.s2 + adj - lane + int64_t(x) * fr.sn;
+      l2_prefetch_cell(src + e, u);
     }
     const int t1 = G1.z, t2 = G2.z;
     const bool in_box = t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p;
