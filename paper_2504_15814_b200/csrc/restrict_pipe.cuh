@@ -35,30 +35,6 @@ __device__ __forceinline__ void l2_prefetch_cell(const double* cell, int u) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(bytes) : "memory");
 }
 
-// decode a restriction item and bulk-prefetch its L x L x L window into L2,
-// one cell per lane
-template <int L>
-__device__ __forceinline__ void prefetch_window(const DevOp& op, const th_face* __restrict__ faces, int64_t item,
-                                                const double* __restrict__ src, int u, int lane) {
-  const int64_t f = item / op.max_items;
-  const th_face* fp = faces + f;
-  FaceRef fr;
-  decode_face(fp, op, fr);
-  int g0, g1, g2;
-  if (!decode_item(op, fr, int(item - f * op.max_items), g0, g1, g2)) return;
-  const int w0 = __ldg(&op.grp0[g0]).x, w1 = __ldg(&op.grp1[g1]).x, w2 = __ldg(&op.grp1[g2]).x;
-  const int p = op.p;
-  const int64_t adj = fr.src0 - __ldg(&fp->src[0]) + int64_t(w0) * fr.sn;
-  for (int cell = lane; cell < L * L * L; cell += 32) {
-    const int x = cell % L, y = (cell / L) % L, z = cell / (L * L);
-    const int a1 = w1 + y, a2 = w2 + z;
-    const int b1 = (a1 >= p) + (a1 >= 2 * p), b2 = (a2 >= p) + (a2 >= 2 * p);
-    const int64_t e = __ldg(&fp->src[b1 + 3 * b2]) + int64_t(a1 - b1 * p) * fr.s1 + int64_t(a2 - b2 * p) * fr.s2 +
-                      adj + int64_t(x) * fr.sn;
-    l2_prefetch_cell(src + e, u);
-  }
-}
-
 template <int MODE, int L, int NCLS>
 struct RestrictParams {
   double w[MODE == 1 ? NCLS : 1][MODE == 1 ? L * L * L : 1][3];  // dense blocks [cls][cell][child]
@@ -86,9 +62,7 @@ __global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
   const int p = op.p;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t total = n_faces * op.max_items;
-  const int64_t first = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (first < total) prefetch_window<L>(op, faces, first, src, u, lane);
-  for (int64_t item = first; item < total; item += nwarps) {
+  for (int64_t item = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; item < total; item += nwarps) {
     const int64_t f = item / op.max_items;
     const th_face* fp = faces + f;
     FaceRef fr;
@@ -108,9 +82,16 @@ __global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
       yb[y] = (a1 >= p) + (a1 >= 2 * p);
       yo[y] = int64_t(a1 - yb[y] * p) * fr.s1;
     }
-    // the window of the warp's NEXT item goes to L2 now, so its slices stream
-    // from L2 one item later while only one slice is held in registers
-    if (item + nwarps < total) prefetch_window<L>(op, faces, item + nwarps, src, u, lane);
+    // L2 bulk prefetch of the whole window (one cell per lane): the slices
+    // below then stream from L2 while only one slice is held in registers
+    for (int cell = lane; cell < L * L * L; cell += 32) {
+      const int x = cell % L, y = (cell / L) % L, z = cell / (L * L);
+      const int a1 = G1.x + y, a2 = G2.x + z;
+      const int b1 = (a1 >= p) + (a1 >= 2 * p), b2 = (a2 >= p) + (a2 >= 2 * p);
+      const int64_t e = __ldg(&fp->src[b1 + 3 * b2]) + int64_t(a1 - b1 * p) * fr.s1 +
+                        int64_t(a2 - b2 * p) * fr.s2 + adj - lane + int64_t(x) * fr.sn;
+      l2_prefetch_cell(src + e, u);
+    }
     const int t1 = G1.z, t2 = G2.z;
     const bool in_box = t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p;
     const int64_t obase = fr.dst + (t1 - fr.lo1) * fr.d1 + (t2 - fr.lo2) * fr.d2 + lane;
