@@ -17,24 +17,6 @@
 // <= NCLS distinct dense blocks; for MODE 2 all tangential rows equal.
 #pragma once
 
-// read-only global load the compiler may not move across the per-slice
-// barrier below (a plain __ldg is treated as a constant read and hoisted,
-// which multiplies the live registers by the window depth and spills)
-__device__ __forceinline__ double ldg_slice(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
-// TMA bulk prefetch of one AoS cell (u doubles) into L2; the range is widened
-// to 16-byte alignment as cp.async.bulk.prefetch requires
-__device__ __forceinline__ void l2_prefetch_cell(const double* cell, int u) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(cell);
-  const uintptr_t lo = a & ~uintptr_t(15);
-  const unsigned bytes = unsigned((a + uintptr_t(u) * 8 - lo + 15) & ~uintptr_t(15));
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(bytes) : "memory");
-}
-
 template <int MODE, int L, int NCLS>
 struct RestrictParams {
   double w[MODE == 1 ? NCLS : 1][MODE == 1 ? L * L * L : 1][3];  // dense blocks [cls][cell][child]

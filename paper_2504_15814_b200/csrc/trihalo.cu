@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
   }
 }
 
+#include "helpers.cuh"
 #include "window.cuh"
 #include "restrict_pipe.cuh"
 
@@ -592,9 +593,9 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   const th::HostOperator& h = op->host;
   const bool interp = h.role == 0;
   bool done = true;
-#define TH_WIN(MODE, L, CT, ORDER, NU, SMEM)                                                           \
+#define TH_WIN(MODE, L, CT, ORDER, NU, SMEM, MINB)                                                     \
   do {                                                                                                 \
-    auto kfn = window_kernel<MODE, L, L, 3, CT, ORDER, NU>;                                          \
+    auto kfn = window_kernel<MODE, L, L, 3, CT, ORDER, NU, MINB>;                                    \
     if (SMEM > 48 * 1024) TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM))); \
     const int64_t units = n_faces * int64_t(op->dev.units_per_face);                                  \
     const int wblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 16));              \
@@ -617,13 +618,13 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2) TH_RREG(2, 3, 1, 2, 5, 10);
   else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 1, 6, 12);
 #undef TH_RREG
-  else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0);
-  else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0);
-  else if (h.fast_mode == 2 && h.fast_L0 == 3 && interp) TH_WIN(2, 3, 3, 0, 1, 0);
-  else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 2, 0);
-  else if (h.fast_mode == 1 && h.fast_L0 == 3 && interp) TH_WIN(1, 3, 3, 0, 2, 0);
-  else if (h.fast_mode == 1 && h.fast_L0 == 3 && !interp && op->smem_ok) TH_WIN(1, 3, 1, 0, 2, op->smem_bytes);
-  else if (h.fast_mode == 1 && h.fast_L0 == 5 && !interp && op->smem_ok) TH_WIN(1, 5, 1, 0, 2, op->smem_bytes);
+  else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0, 3);
+  else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0, 3);
+  else if (h.fast_mode == 2 && h.fast_L0 == 3 && interp) TH_WIN(2, 3, 3, 0, 1, 0, 3);
+  else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 2, 0, 3);
+  else if (h.fast_mode == 1 && h.fast_L0 == 3 && interp) TH_WIN(1, 3, 3, 0, 2, 0, 2);
+  else if (h.fast_mode == 1 && h.fast_L0 == 3 && !interp && op->smem_ok) TH_WIN(1, 3, 1, 0, 2, op->smem_bytes, 2);
+  else if (h.fast_mode == 1 && h.fast_L0 == 5 && !interp && op->smem_ok) TH_WIN(1, 5, 1, 0, 2, op->smem_bytes, 2);
   else done = false;
 #undef TH_WIN
   if (done) {

@@ -45,8 +45,8 @@ __device__ __forceinline__ void gacc(double& acc, double g, double v) {
   else if (g != 0.0) acc = fma(g, v, acc);
 }
 
-template <int MODE, int L0, int LT, int C0, int CT, int ORDER, int NU>
-__global__ void __launch_bounds__(128) window_kernel(DevOp op, const double* __restrict__ src,
+template <int MODE, int L0, int LT, int C0, int CT, int ORDER, int NU, int MINB>
+__global__ void __launch_bounds__(128, MINB) window_kernel(DevOp op, const double* __restrict__ src,
                                                      double* __restrict__ dst, const th_face* __restrict__ faces,
                                                      int64_t n_faces, int u, int32_t* flag) {
   constexpr int S = L0 * LT * LT;
@@ -118,6 +118,11 @@ __global__ void __launch_bounds__(128) window_kernel(DevOp op, const double* __r
     // ---- walk the t2 groups of the box ----------------------------------------
     for (int g2 = fr.g2; g2 < fr.g2 + fr.n2; ++g2) {
       const int4 G2 = __ldg(&op.grp1[g2]);
+      // bulk-prefetch this block's window into L2 (one cell per lane): the
+      // slices below then stream from L2 with one slice held in registers
+      for (int cell = lane; cell < S; cell += 32)
+        l2_prefetch_cell(src + src_addr(fp, op, fr, G0.x + cell % L0, G1.x + (cell / L0) % LT, G2.x + cell / (L0 * LT)),
+                         u);
       int64_t zrow[LT];  // source offset of (x = 0, y = 0 block column, z) without the y part
       int zb[LT];
 #pragma unroll
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(128) window_kernel(DevOp op, const double* __r
 #pragma unroll
             for (int x = 0; x < L0; ++x)
 #pragma unroll
-              for (int q = 0; q < NU; ++q) v[y][x][q] = okq[q] ? __ldg(src + base + xo[x] + 32 * q) : 0.0;
+              for (int q = 0; q < NU; ++q) v[y][x][q] = okq[q] ? ldg_slice(src + base + xo[x] + 32 * q) : 0.0;
           }
           double T[NT][NU];
 #pragma unroll
@@ -252,6 +257,7 @@ __global__ void __launch_bounds__(128) window_kernel(DevOp op, const double* __r
 #pragma unroll
                   for (int q = 0; q < NU; ++q) acc[mi][q] = fma(pz[c], T[t][q], acc[mi][q]);
           }
+          asm volatile("" ::: "memory");  // one slice of loads live at a time
         }
         // ---- store ------------------------------------------------------------
         bool bad = false;
