@@ -34,6 +34,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink patch / face counts (tuning runs only)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
@@ -130,7 +131,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    wl = W.build(args.config, rank=rank)
+    wl = W.build(args.config, rank=rank, scale=args.scale)
     s = wl.spec
     p, k, u = s.p, s.k, s.u
     passes = []

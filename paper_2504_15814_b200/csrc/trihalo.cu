@@ -44,6 +44,7 @@ int32_t fail(int32_t code, const std::string& msg, int col = -1) {
 // ---------------------------------------------------------------------------
 struct DevOp {
   int32_t role, scheme, p, k;
+  int32_t prefetch;    // L2 bulk prefetch of block windows (TH_PREFETCH=0 disables; tuning)
   int32_t ns0;         // source extent along the normal (2k)
   int32_t G0, G1;      // groups along normal / tangential
   int32_t max_items;   // work items per face (upper bound)
@@ -504,6 +505,10 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   op->max_children *= mc1 * mc1;
   op->on_device = upload_to_device;
   d.n_blocks = (int32_t)h.block_off.size();
+  {
+    const char* e = std::getenv("TH_PREFETCH");
+    d.prefetch = e ? std::atoi(e) : 1;
+  }
   d.units_per_face = 0;
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b)

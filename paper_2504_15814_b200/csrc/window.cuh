@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128, MINB) window_kernel(DevOp op, const doubl
       const int4 G2 = __ldg(&op.grp1[g2]);
       // bulk-prefetch this block's window into L2 (one cell per lane): the
       // slices below then stream from L2 with one slice held in registers
-      for (int cell = lane; cell < S; cell += 32)
+      for (int cell = lane; op.prefetch && cell < S; cell += 32)
         l2_prefetch_cell(src + src_addr(fp, op, fr, G0.x + cell % L0, G1.x + (cell / L0) % LT, G2.x + cell / (L0 * LT)),
                          u);
       int64_t zrow[LT];  // source offset of (x = 0, y = 0 block column, z) without the y part
