@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
     }
     // L2 bulk prefetch of the whole window (one cell per lane): the slices
     // below then stream from L2 while only one slice is held in registers
-    for (int cell = lane; op.prefetch && cell < L * L * L; cell += 32) {
+    // (3x3x3 windows only: for 5x5x5 windows the 125 TMA prefetch ops per item
+    //  cost more than they save, measured 0.38 vs 0.47 of HBM on config 3)
+    for (int cell = lane; L == 3 && op.prefetch && cell < L * L * L; cell += 32) {
       const int x = cell % L, y = (cell / L) % L, z = cell / (L * L);
       const int a1 = G1.x + y, a2 = G2.x + z;
       const int b1 = (a1 >= p) + (a1 >= 2 * p), b2 = (a2 >= p) + (a2 >= 2 * p);
