@@ -230,6 +230,136 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+def run_multi(args, rank, world, local_rank):
+    """Config 5: 32,768 coarse patches block-partitioned over the ranks, 196,608 faces,
+    order3 interpolation + restriction of every face, fine patches drawn from the pool
+    by index lists, 10% of faces with their fine patches on another rank (results of
+    those cross NVLink in one grouped NCCL send/recv step, overlapped with local faces).
+    Strong scaling: the job is fixed, ranks split it."""
+    import torch
+
+    import paper_2504_15814_b200 as th
+    import workloads as W
+    from paper_2504_15814_b200.multigpu import GpuCompute, Sweep, plan_sweep
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    wl = W.build_multi(world, rank, scale=args.scale)
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    plans = plan_sweep(wl.part, wl.coarse, wl.fine, wl.segment, rank)
+    per = k * p * p * u
+    lo = int(wl.part.bounds[rank])
+    ops = {role: th.operators.DEFAULT_CACHE.device_operator(role, "order3", p, k) for role in plans}
+
+    def make_records(role, ids):
+        if role == "interpolate":
+            return th.pool_interp_faces(p, k, u, wl.coarse[ids] - lo, wl.normal[ids], wl.side[ids], wl.segment[ids])
+        return th.pool_restrict_faces(p, k, u, wl.fine[ids] - lo, wl.normal[ids], wl.side[ids])
+
+    comp = GpuCompute(plans, make_records, ops, {"interpolate": wl.pool, "restrict": wl.pool}, u)
+    sweep = Sweep(plans, per, dev, torch.float64)
+    for _ in range(max(3, args.warmup)):
+        sweep.run(comp)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.05)
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0.record(stream)
+    for _ in range(args.steps):
+        sweep.run(comp)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    n_faces = s.n_faces
+    values = 2 * n_faces * per
+    b_i, f_i, _ = unit_costs("interpolate", "order3", p, k, u, list(range(9)))
+    b_r, f_r, _ = unit_costs("restrict", "order3", p, k, u, [None])
+    step_bytes = n_faces * (b_i + b_r) / world
+    peak, peak_kind = peaks()
+    cross = {r: int(sum(x.size for x in pl.send)) for r, pl in plans.items()}
+    res = {
+        "metric": METRIC, "value": values / (ms / 1e3), "unit": "values/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic cubic field + 1e-6 noise in HBM; fine patches drawn from the pool by index lists",
+        "config": {"workload": f"config5: {s.name}", "p": p, "k": k, "u": u, "coarse_patches": s.n_patches,
+                   "faces": n_faces, "passes": ["interpolate:order3", "restrict:order3"],
+                   "parallelism": f"{world} ranks, block-partitioned patches, NCCL P2P for cross faces",
+                   "cross_faces_sent_rank0": cross},
+        "roofline": {"bound": "hbm", "kernel": "interpolate+restrict:order3 (whole sweep, per rank)",
+                     "achieved": round(step_bytes / (ms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(step_bytes / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"},
+        "gpu_launches": args.steps * comp.launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu:
+        res["parity"] = multi_parity(wl, plans, sweep, per)
+    return res
+
+
+def multi_parity(wl, plans, sweep, per, n_sample=24):
+    """Oracle check of a sample of faces computed and kept on this rank."""
+    from oracle import exchange as OE
+    from oracle import geometry as OG
+
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    E = p + 2 * k
+    lo = int(wl.part.bounds[0])
+    pool = wl.pool.view(-1, E, E, E, u)
+    rng = np.random.default_rng(5)
+    worst = 0.0
+    for role, plan in plans.items():
+        pick = rng.choice(plan.local.size, min(n_sample, plan.local.size), replace=False)
+        for j in pick:
+            f = int(plan.local[j])
+            n, sd = int(wl.normal[f]), int(wl.side[f])
+            t1, t2 = [d for d in range(3) if d != n]
+            if role == "interpolate":
+                lo3, ext = [k, k, k], [p, p, p]
+                lo3[n], ext[n] = (p if sd == 0 else 0), 2 * k
+                c = int(wl.coarse[f]) - lo
+                src = pool[c, lo3[2]:lo3[2] + ext[2], lo3[1]:lo3[1] + ext[1], lo3[0]:lo3[0] + ext[0]].cpu().numpy().reshape(-1)
+                seg = int(wl.segment[f])
+            else:
+                ext = [3 * p, 3 * p, 3 * p]
+                ext[n] = 2 * k
+                world_box = np.zeros((ext[2], ext[1], ext[0], u))
+                for b in range(9):
+                    lo3, e = [k, k, k], [p, p, p]
+                    lo3[n], e[n] = (0 if sd == 0 else p), 2 * k
+                    blk = pool[int(wl.fine[f, b]) - lo, lo3[2]:lo3[2] + e[2], lo3[1]:lo3[1] + e[1],
+                               lo3[0]:lo3[0] + e[0]].cpu().numpy()
+                    off = [0, 0, 0]
+                    off[t1], off[t2] = (b % 3) * p, (b // 3) * p
+                    world_box[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = blk
+                src = world_box.reshape(-1)
+                seg = 0
+            cfg = OG.FaceCfg("xyz"[n], ("negative", "positive")[sd], seg, p, k, u)
+            ex = OE.exchange_for(cfg, "order3", role)
+            want = np.empty(ex.n_out)
+            ex.run(src, want)
+            got = sweep.out[role][j * per:(j + 1) * per].cpu().numpy()
+            worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))
+    return {"sample_faces": 2 * n_sample, "max_rel_err": worst, "tol": 1e-12, "ok": worst <= 1e-12}
+
+
 def run_e2e(args, wl, passes, dev, world):
     """Same metric through the C ABI with HOST buffers: every step copies each face's
     reference source buffer (pinned host -> HBM), applies all passes, copies the results
@@ -459,7 +589,7 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = run_ours(args, rank, world, local_rank)
+    res = run_multi(args, rank, world, local_rank) if args.config == 5 else run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

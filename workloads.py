@@ -323,3 +323,66 @@ def face_cfg(wl: Workload, f: int) -> th.FaceConfig:
     s = wl.spec
     return th.FaceConfig("xyz"[wl.faces.normal[f]], ("negative", "positive")[wl.faces.side[f]],
                          int(wl.faces.segment[f]), s.p, s.k, s.u)
+
+
+# ---------------------------------------------------------------------------
+# config 5: patches block-partitioned over ranks, fine patches drawn from the
+# pool via index lists, 10% of faces with their fine patches on another rank
+# ---------------------------------------------------------------------------
+
+@dataclass
+class MultiWorkload:
+    spec: Spec
+    fld: Field
+    part: object
+    coarse: np.ndarray
+    normal: np.ndarray
+    side: np.ndarray
+    segment: np.ndarray
+    fine: np.ndarray          # (n_faces, 9) global patch ids, one owner per face
+    m: int
+    H: float
+    pool: object = None       # this rank's patches [lo, hi)
+
+
+def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10) -> MultiWorkload:
+    """Global face list of config 5 (identical on every rank)."""
+    from paper_2504_15814_b200.multigpu import Partition
+
+    spec = SPECS[5]
+    if scale != 1.0:
+        spec = Spec(**{**spec.__dict__, "n_patches": max(8 * world, int(spec.n_patches * scale)),
+                       "n_faces": max(12, int(spec.n_faces * scale))})
+    rng = np.random.default_rng(spec.seed)
+    fld = Field.make(spec.field, spec.u, rng)
+    n, nf = spec.n_patches, spec.n_faces
+    part = Partition(n, world)
+    coarse = rng.integers(0, n, nf)
+    orient = rng.integers(0, 6, nf)
+    segment = rng.integers(0, 9, nf)
+    c_own = part.owner(coarse)
+    f_own = c_own.copy()
+    if world > 1:
+        flip = rng.random(nf) < cross
+        f_own[flip] = (c_own[flip] + rng.integers(1, world, int(flip.sum()))) % world
+    lo = part.bounds[f_own]
+    size = part.bounds[f_own + 1] - lo
+    fine = lo[:, None] + (rng.random((nf, 9)) * size[:, None]).astype(np.int64)
+    m = lattice(n)
+    return MultiWorkload(spec, fld, part, coarse.astype(np.int64), (orient // 2).astype(np.int64),
+                         (orient % 2).astype(np.int64), segment.astype(np.int64), fine, m, 1.0 / (m * spec.p))
+
+
+def build_multi(world: int, rank: int, scale: float = 1.0) -> MultiWorkload:
+    import torch
+
+    wl = describe_multi(world, scale)
+    s = wl.spec
+    E = s.p + 2 * s.k
+    lo, hi = int(wl.part.bounds[rank]), int(wl.part.bounds[rank + 1])
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(s.seed + 7919 * rank)
+    wl.pool = torch.empty(max(1, (hi - lo) * E ** 3 * s.u), dtype=torch.float64, device="cuda")
+    _fill(wl.pool, lambda a, b: patch_cell_centres(s, wl.m, wl.H, np.arange(lo + a, lo + b)), hi - lo, E ** 3,
+          wl.fld, s.u, gen)
+    return wl
