@@ -266,8 +266,9 @@ void choose_fast_path(HostOperator& op) {
   op.fast_CT = CT;
   if (op.scheme == 0) {
     op.fast_mode = 2;
-  } else if (interp && op.scheme >= 2) {
-    op.fast_mode = 3;
+  }
+  if (op.scheme >= 2) {  // Gram synthesis tables for both roles (full windows checked above)
+    op.gram_ok = true;
     const int order = op.scheme;
     for (int a = 0; a < 2; ++a) {
       const AxisGeom& g = op.ax[a];
@@ -281,6 +282,10 @@ void choose_fast_path(HostOperator& op) {
           }
       }
     }
+  }
+  if (op.scheme == 0) {
+  } else if (interp && op.scheme >= 2) {
+    op.fast_mode = 3;
   } else {
     // dense blocks are laid out with the real child counts: the fixed-window
     // kernel indexes them as C0 x CT x CT, so every group must be full

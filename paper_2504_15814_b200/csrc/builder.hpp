@@ -68,7 +68,9 @@ struct HostOperator {
   int fast_mode = 0;  // 0 none, 1 dense blocks, 2 tensor rows, 3 Gram-separable least squares
   int fast_L0 = 0, fast_LT = 0, fast_C0 = 0, fast_CT = 0;
   // Gram synthesis values per group: [child < 3][degree < 4] = P_a(e_child) / |P_a|^2
+  // (filled for every Taylor operator whose windows are all full: gram_ok)
   std::vector<double> synth[2];
+  bool gram_ok = false;
   double max_condition = 0.0;
   int n_condition_warnings = 0;
   std::vector<std::string> condition_warnings;

@@ -1,0 +1,184 @@
+// Gram sliding kernel for the least-squares schemes (order2 / order3), both
+// roles (included by trihalo.cu after window.cuh).
+//
+// The reference row of a target cell is its least-squares fit over a full
+// tensor window, evaluated at the target (taylor.py:171-219).  That fit is the
+// orthogonal projection onto total degree <= ORDER, so it can be computed with
+// the window's discrete Gram polynomials, separably:
+//   x (normal) moments per source line    m_a      = sum_x P_a(x) v
+//   y (t1) moments per window and slice   T_ab(a2) = sum_y P_b(y) m_a
+//   z (t2) moments per block              M_abc    = sum_z P_c(z) T_ab(w2 + z)
+//   synthesis at the children             out      = sum S0[a] S1[b] S2[c] M_abc
+// with S_d = P(e)/|P|^2 from the builder (builder.cpp choose_fast_path).
+// Integer Gram weights are immediates: no weight loads at all.
+//
+// One warp owns a work unit = (face, t1 group, 32-unknown chunk) and walks the
+// face's t2 groups.  Consecutive blocks' windows overlap along t2 (by 4 of 5
+// slices for interpolation, 2 of 5 for restriction), so each source slice is
+// loaded and x/y-projected once into a per-lane ring of L moment slices in
+// shared memory; a block then only does its z-pass and synthesis.
+#pragma once
+
+template <int ORDER, int ROLE, int MINB>
+__global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const double* __restrict__ src,
+                                                               double* __restrict__ dst,
+                                                               const th_face* __restrict__ faces, int64_t n_faces,
+                                                               int u, int32_t* flag) {
+  constexpr int L = ORDER == 2 ? 3 : 5;
+  constexpr int D = ORDER + 1;
+  constexpr int NT = ORDER == 2 ? 6 : 10;   // pairs a + b <= ORDER
+  constexpr int NM = ORDER == 2 ? 10 : 20;  // triples a + b + c <= ORDER
+  constexpr int C0 = 3, CT = ROLE == 0 ? 3 : 1;
+  extern __shared__ double ring_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* const ring = ring_all + warp * (L * NT * 32) + lane;  // [slot][t] x 32 lanes, lane-private
+  const int p = op.p;
+  const int upf = op.units_per_face;
+  const int nch = (u + 31) / 32;
+  const int64_t total = n_faces * upf * nch;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t unit = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; unit < total; unit += nw) {
+    const int64_t fu = unit / nch;
+    const int cb = int(unit - fu * nch) * 32;
+    const int64_t f = fu / upf;
+    const int r = int(fu - f * upf);
+    const th_face* fp = faces + f;
+    FaceRef fr;
+    decode_face(fp, op, fr);
+    if (r >= fr.n0 * fr.n1) continue;
+    const int g1 = fr.g1 + r % fr.n1, g0 = fr.g0 + r / fr.n1;
+    const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]);
+    const bool ok = cb + lane < u;
+    // source line bases per t1 row y (restriction adds the fine block of (y, z))
+    const int64_t adj = ROLE == 0 ? 0 : fr.src0 - __ldg(&fp->src[0]);
+    int64_t ybase[L];
+    int yb[L];
+#pragma unroll
+    for (int y = 0; y < L; ++y) {
+      const int a1 = G1.x + y;
+      yb[y] = ROLE == 0 ? 0 : (a1 >= p) + (a1 >= 2 * p);
+      ybase[y] = (ROLE == 0 ? fr.src0 : adj) + int64_t(a1 - yb[y] * p) * fr.s1 + int64_t(G0.x) * fr.sn + cb + lane;
+    }
+    // target offsets of the normal and t1 children
+    int64_t do0[C0], do1[CT];
+    bool ok0[C0], ok1[CT];
+#pragma unroll
+    for (int i = 0; i < C0; ++i) {
+      const int t = G0.z + i;
+      ok0[i] = i < G0.w && t >= fr.lo0 && t < fr.hi0;
+      do0[i] = int64_t(t - fr.lo0) * fr.dn;
+    }
+#pragma unroll
+    for (int i = 0; i < CT; ++i) {
+      const int t = G1.z + i;
+      ok1[i] = i < G1.w && t >= fr.lo1 && t < fr.lo1 + p;
+      do1[i] = int64_t(t - fr.lo1) * fr.d1;
+    }
+    const double* s0 = op.synth0 + g0 * 12;
+    const double* s1 = op.synth1 + g1 * 12;
+    int hi = -1;  // highest t2 source slice held in the ring
+    for (int g2 = fr.g2; g2 < fr.g2 + fr.n2; ++g2) {
+      const int4 G2 = __ldg(&op.grp1[g2]);
+      const int w2 = G2.x;
+      // ---- new source slices: load, x-pass, y-pass, into the ring ----------
+#pragma unroll 1
+      for (int a2 = max(hi + 1, w2); a2 < w2 + L; ++a2) {
+        const int b2 = ROLE == 0 ? 0 : (a2 >= p) + (a2 >= 2 * p);
+        const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
+        double v[L][L];
+#pragma unroll
+        for (int y = 0; y < L; ++y) {
+          const int64_t base = ybase[y] + zo + (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * b2]));
+#pragma unroll
+          for (int x = 0; x < L; ++x) v[y][x] = ok ? ldg_slice(src + base + int64_t(x) * fr.sn) : 0.0;
+        }
+        double T[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) T[t] = 0.0;
+#pragma unroll
+        for (int y = 0; y < L; ++y) {
+          double m[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            m[a] = 0.0;
+#pragma unroll
+            for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[y][x]);
+          }
+          int t = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
+        }
+        double* slot = ring + (a2 % L) * (NT * 32);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) slot[t * 32] = T[t];
+        asm volatile("" ::: "memory");  // one slice of loads live at a time
+      }
+      hi = max(hi, w2 + L - 1);
+      // ---- z-pass of this block -------------------------------------------------
+      double M[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) M[i] = 0.0;
+      int slot0 = w2 % L;
+#pragma unroll
+      for (int z = 0; z < L; ++z) {
+        const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
+        const double* slot = ring + sl * (NT * 32);
+        int t = 0, mi = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b + a < D; ++b, ++t) {
+            const double Tz = slot[t * 32];
+#pragma unroll
+            for (int c = 0; c + b + a < D; ++c, ++mi) gacc(M[mi], Gram<L>::P(c, z), Tz);
+          }
+      }
+      // ---- synthesis at the children and store -----------------------------------
+      const double* s2 = op.synth1 + g2 * 12;
+      bool bad = false;
+      double* const dbase = dst + fr.dst + cb + lane;
+#pragma unroll
+      for (int l = 0; l < CT; ++l) {
+        const int tz = G2.z + l;
+        if (!(l < G2.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
+        const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
+        double Q[NT];
+        int t = 0, mi = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b + a < D; ++b, ++t) {
+            Q[t] = 0.0;
+#pragma unroll
+            for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(__ldg(s2 + l * 4 + c), M[mi], Q[t]);
+          }
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+          if (!ok1[j]) continue;
+          double R[D];
+          int tt = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            R[a] = 0.0;
+#pragma unroll
+            for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + j * 4 + b), Q[tt], R[a]);
+          }
+#pragma unroll
+          for (int i = 0; i < C0; ++i) {
+            if (!ok0[i]) continue;
+            double o = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
+            if (ok) {
+              dbase[do0[i] + do1[j] + do2] = o;
+              bad |= !isfinite(o);
+            }
+          }
+        }
+      }
+      raise_flag(flag, bad);
+    }
+  }
+}

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "helpers.cuh"
 #include "window.cuh"
 #include "restrict_pipe.cuh"
+#include "gram_slide.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -616,7 +617,23 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   } while (0)
   // TH_RESTRICT_NU=1 selects the one-unknown-per-lane variant (tuning experiments)
   static const int rnu = [] { const char* e = std::getenv("TH_RESTRICT_NU"); return e && e[0] == '1' ? 1 : 2; }();
-  if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
+#define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
+  do {                                                                                                 \
+    auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
+    const size_t smem = size_t(4) * (ORDER == 2 ? 3 * 6 : 5 * 10) * 32 * 8;                            \
+    if (smem > 48 * 1024) TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
+    const int64_t units = n_faces * int64_t(op->dev.units_per_face) * ((u + 31) / 32);                 \
+    const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * MINB * 2));       \
+    kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                        \
+  } while (0)
+  // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 1; }();
+  const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
+  if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
+  else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
+#undef TH_GRAM
+  else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
   else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 1, 6, 12);
   else if (op->r_mode == 1 && op->r_L == 5 && rnu == 2) TH_RREG(1, 5, 9, 2, 4, 8);
   else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 1, 5, 10);
