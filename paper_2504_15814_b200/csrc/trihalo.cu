@@ -627,7 +627,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                        \
   } while (0)
   // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 1; }();
+  // (bit 1: interpolation, bit 2: order3 restriction)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 3; }();
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
