@@ -85,6 +85,14 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
       for (int a2 = max(hi + 1, w2); a2 < w2 + L; ++a2) {
         const int b2 = ROLE == 0 ? 0 : (a2 >= p) + (a2 >= 2 * p);
         const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
+        // L2 bulk prefetch of the next slice (one cell per lane) while this one is projected
+        if (op.prefetch && lane < L * L && a2 + 1 < op.ns_t) {
+          const int x = lane % L, y = lane / L, an = a2 + 1;
+          const int bn = ROLE == 0 ? 0 : (an >= p) + (an >= 2 * p);
+          const int64_t e = ybase[y] - (cb + lane) + int64_t(an - bn * p) * fr.s2 + int64_t(x) * fr.sn +
+                            (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * bn]));
+          l2_prefetch_cell(src + e, u);
+        }
         double v[L][L];
 #pragma unroll
         for (int y = 0; y < L; ++y) {

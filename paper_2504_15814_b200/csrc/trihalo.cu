@@ -62,6 +62,7 @@ struct DevOp {
   const double* synth1;
   int32_t n_blocks;
   int32_t units_per_face;   // (normal group, t1 group) columns per face, fixed-window kernels
+  int32_t ns_t;             // source extent along a tangential axis
   int32_t seg_g[3][2];
   int32_t half_g[3][2];
   int32_t half_t[3][2];
@@ -511,6 +512,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
     d.prefetch = e ? std::atoi(e) : 1;
   }
   d.units_per_face = 0;
+  d.ns_t = h.ax[1].ns;
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b)
       d.units_per_face = std::max(d.units_per_face, (h.half_g[a][1] - h.half_g[a][0]) * (h.seg_g[b][1] - h.seg_g[b][0]));
