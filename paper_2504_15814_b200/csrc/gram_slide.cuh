@@ -9,18 +9,14 @@
 //   y (t1) moments per window and slice   T_ab(a2) = sum_y P_b(y) m_a
 //   z (t2) moments per block              M_abc    = sum_z P_c(z) T_ab(w2 + z)
 //   synthesis at the children             out      = sum S0[a] S1[b] S2[c] M_abc
-// with S_d = P(e)/|P|^2 from the builder (builder.cpp choose_fast_path), read
-// with non-hoistable loads at each use (hoisted, they pin ~50 registers).
+// with S_d = P(e)/|P|^2 from the builder (builder.cpp choose_fast_path).
 // Integer Gram weights are immediates: no weight loads at all.
 //
-// One warp owns a work unit = (face, t1 group, 32-unknown chunk) and streams
-// the t2 source slices its blocks need, in order.  Consecutive blocks' windows
-// overlap along t2 (4 of 5 slices for interpolation, 2 of 5 for restriction),
-// so each slice is loaded and x/y-projected once into a per-lane ring of L
-// moment slices in shared memory; a block whose window is complete then only
-// does its z-pass and synthesis.  Slice a2+1 is loaded into registers before
-// slice a2 is projected (two register buffers), so every warp keeps a slice of
-// loads in flight.
+// One warp owns a work unit = (face, t1 group, 32-unknown chunk) and walks the
+// face's t2 groups.  Consecutive blocks' windows overlap along t2 (by 4 of 5
+// slices for interpolation, 2 of 5 for restriction), so each source slice is
+// loaded and x/y-projected once into a per-lane ring of L moment slices in
+// shared memory; a block then only does its z-pass and synthesis.
 #pragma once
 
 template <int ORDER, int ROLE, int MINB>
@@ -80,46 +76,59 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
     }
     const double* s0 = op.synth0 + g0 * 12;
     const double* s1 = op.synth1 + g1 * 12;
-
-    auto load_slice = [&](int a2, double (&v)[L][L]) {
-      const int b2 = ROLE == 0 ? 0 : (a2 >= p) + (a2 >= 2 * p);
-      const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
-#pragma unroll
-      for (int y = 0; y < L; ++y) {
-        const int64_t base = ybase[y] + zo + (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * b2]));
-#pragma unroll
-        for (int x = 0; x < L; ++x) v[y][x] = ok ? ldg_slice(src + base + int64_t(x) * fr.sn) : 0.0;
-      }
-    };
-    auto project = [&](int a2, const double (&v)[L][L]) {
-      double T[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) T[t] = 0.0;
-#pragma unroll
-      for (int y = 0; y < L; ++y) {
-        double m[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          m[a] = 0.0;
-#pragma unroll
-          for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[y][x]);
+    int hi = -1;  // highest t2 source slice held in the ring
+    for (int g2 = fr.g2; g2 < fr.g2 + fr.n2; ++g2) {
+      const int4 G2 = __ldg(&op.grp1[g2]);
+      const int w2 = G2.x;
+      // ---- new source slices: load, x-pass, y-pass, into the ring ----------
+#pragma unroll 1
+      for (int a2 = max(hi + 1, w2); a2 < w2 + L; ++a2) {
+        const int b2 = ROLE == 0 ? 0 : (a2 >= p) + (a2 >= 2 * p);
+        const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
+        // L2 bulk prefetch of the next slice (one cell per lane) while this one is projected
+        if (op.prefetch && lane < L * L && a2 + 1 < op.ns_t) {
+          const int x = lane % L, y = lane / L, an = a2 + 1;
+          const int bn = ROLE == 0 ? 0 : (an >= p) + (an >= 2 * p);
+          const int64_t e = ybase[y] - (cb + lane) + int64_t(an - bn * p) * fr.s2 + int64_t(x) * fr.sn +
+                            (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * bn]));
+          l2_prefetch_cell(src + e, u);
         }
-        int t = 0;
+        double v[L][L];
 #pragma unroll
-        for (int a = 0; a < D; ++a)
+        for (int y = 0; y < L; ++y) {
+          const int64_t base = ybase[y] + zo + (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * b2]));
 #pragma unroll
-          for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
+          for (int x = 0; x < L; ++x) v[y][x] = ok ? ldg_slice(src + base + int64_t(x) * fr.sn) : 0.0;
+        }
+        double T[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) T[t] = 0.0;
+#pragma unroll
+        for (int y = 0; y < L; ++y) {
+          double m[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            m[a] = 0.0;
+#pragma unroll
+            for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[y][x]);
+          }
+          int t = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
+        }
+        double* slot = ring + (a2 % L) * (NT * 32);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) slot[t * 32] = T[t];
+        asm volatile("" ::: "memory");  // one slice of loads live at a time
       }
-      double* slot = ring + (a2 % L) * (NT * 32);
-#pragma unroll
-      for (int t = 0; t < NT; ++t) slot[t * 32] = T[t];
-    };
-    auto finish = [&](int g2, int w2, const int4& G2) {
-      // z-pass over the ring, synthesis at the children, store
+      hi = max(hi, w2 + L - 1);
+      // ---- z-pass of this block -------------------------------------------------
       double M[NM];
 #pragma unroll
       for (int i = 0; i < NM; ++i) M[i] = 0.0;
-      const int slot0 = w2 % L;
+      int slot0 = w2 % L;
 #pragma unroll
       for (int z = 0; z < L; ++z) {
         const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
@@ -134,6 +143,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             for (int c = 0; c + b + a < D; ++c, ++mi) gacc(M[mi], Gram<L>::P(c, z), Tz);
           }
       }
+      // ---- synthesis at the children and store -----------------------------------
       const double* s2 = op.synth1 + g2 * 12;
       bool bad = false;
       double* const dbase = dst + fr.dst + cb + lane;
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
           for (int b = 0; b + a < D; ++b, ++t) {
             Q[t] = 0.0;
 #pragma unroll
-            for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(ldg_slice(s2 + l * 4 + c), M[mi], Q[t]);
+            for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(__ldg(s2 + l * 4 + c), M[mi], Q[t]);
           }
 #pragma unroll
         for (int j = 0; j < CT; ++j) {
@@ -161,14 +171,14 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
           for (int a = 0; a < D; ++a) {
             R[a] = 0.0;
 #pragma unroll
-            for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(ldg_slice(s1 + j * 4 + b), Q[tt], R[a]);
+            for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + j * 4 + b), Q[tt], R[a]);
           }
 #pragma unroll
           for (int i = 0; i < C0; ++i) {
             if (!ok0[i]) continue;
             double o = 0.0;
 #pragma unroll
-            for (int a = 0; a < D; ++a) o = fma(ldg_slice(s0 + i * 4 + a), R[a], o);
+            for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
             if (ok) {
               dbase[do0[i] + do1[j] + do2] = o;
               bad |= !isfinite(o);
@@ -177,33 +187,6 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         }
       }
       raise_flag(flag, bad);
-    };
-
-    // ---- stream the t2 slices of all blocks in order ------------------------------
-    // windows of consecutive groups advance monotonically without gaps, so the
-    // slices needed are exactly [w2(first), w2(last) + L)
-    int g2n = fr.g2;  // next block to complete
-    const int g2e = fr.g2 + fr.n2;
-    if (g2n >= g2e) continue;
-    int4 Gn = __ldg(&op.grp1[g2n]);
-    const int a_begin = Gn.x, a_end = __ldg(&op.grp1[g2e - 1]).x + L;
-    double v[2][L][L];
-    load_slice(a_begin, v[0]);
-#pragma unroll 1
-    for (int a2 = a_begin; a2 < a_end; a2 += 2) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int a = a2 + h;
-        if (a < a_end) {
-          if (a + 1 < a_end) load_slice(a + 1, v[1 - h]);
-          project(a, v[h]);
-          while (g2n < g2e && Gn.x + L - 1 == a) {
-            finish(g2n, Gn.x, Gn);
-            if (++g2n < g2e) Gn = __ldg(&op.grp1[g2n]);
-          }
-          asm volatile("" ::: "memory");  // the next slice's loads stay one slice ahead
-        }
-      }
     }
   }
 }

@@ -632,9 +632,9 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   // (bit 1: interpolation, bit 2: order3 restriction)
   static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 3; }();
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
-  if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 4);
-  else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 2);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 3);
+  if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
+  else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
 #undef TH_GRAM
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
   else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 1, 6, 12);
