@@ -19,3 +19,14 @@ __device__ __forceinline__ void l2_prefetch_cell(const double* cell, int u) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(bytes) : "memory");
 }
 
+
+// 8-byte asynchronous global -> shared copy (LDGSTS); the cells of the unpadded
+// AoS layout are only 8-byte aligned, so 16-byte cp.async / TMA do not apply
+__device__ __forceinline__ void cp_async8(unsigned smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_dst), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}

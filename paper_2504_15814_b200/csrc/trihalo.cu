@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "window.cuh"
 #include "restrict_pipe.cuh"
 #include "gram_slide.cuh"
+#include "gram_restrict.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -630,10 +631,21 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   } while (0)
   // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
   // (bit 1: interpolation, bit 2: order3 restriction)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 3; }();
+  // (bit 4: order3 restriction through the asynchronous slice pipeline, gram_restrict.cuh)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 5; }();
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->r_mode == 1 && op->r_L == 5) {
+    // one normal group of 3 children, 1-child tangential groups (checked by prepare_restrict)
+    constexpr int NST = 4;
+    auto kfn = gram_restrict3_kernel<NST, 2>;
+    const size_t smem = size_t(4) * NST * 25 * 32 * 8;
+    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t units = n_faces * int64_t(op->dev.G1) * ((u + 31) / 32);
+    const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 2));
+    kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  }
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
 #undef TH_GRAM
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
