@@ -632,12 +632,14 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
   // (bit 1: interpolation, bit 2: order3 restriction)
   // (bit 4: order3 restriction through the asynchronous slice pipeline, gram_restrict.cuh)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 5; }();
+  //  experimental, off by default: measured 0.30 vs 0.37 of HBM for bit 2 on config 3)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 3; }();
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->r_mode == 1 && op->r_L == 5) {
-    // one normal group of 3 children, 1-child tangential groups (checked by prepare_restrict)
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->r_mode == 1 && op->r_L == 5 && h.p >= 4) {
+    // one normal group of 3 children, 1-child tangential groups (checked by prepare_restrict);
+    // p >= 4 so that a fine slice feeds at most two coarse columns
     constexpr int NST = 4;
     auto kfn = gram_restrict3_kernel<NST, 2>;
     const size_t smem = size_t(4) * NST * 25 * 32 * 8;
