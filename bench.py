@@ -361,78 +361,109 @@ def multi_parity(wl, plans, sweep, per, n_sample=24):
 
 
 def run_e2e(args, wl, passes, dev, world):
-    """Same metric through the C ABI with HOST buffers: every step copies each face's
-    reference source buffer (pinned host -> HBM), applies all passes, copies the results
-    back; chunked over 3 streams so PCIe traffic overlaps the kernels."""
+    """Same metric through the C ABI with HOST buffers: every step ships each face's
+    reference source buffer (pinned host, world layout) to HBM, applies all passes and
+    copies the results back, chunked over 3 streams so PCIe overlaps the kernels.  Only
+    the normal layers the operators read are shipped (th_operator_support_layers:
+    3 of the 6 source layers for linear / order2), one strided cudaMemcpy2D/3DAsync per
+    (chunk, orientation) group via th_copy_box_layers."""
+    import ctypes
+
     import torch
 
     import paper_2504_15814_b200 as th
     import workloads as W
+    from paper_2504_15814_b200 import _native
 
+    lib = _native.load()
     s = wl.spec
     p, k, u = s.p, s.k, s.u
-    # host copies of the per-face reference source buffers
-    n_i, n_r = wl.interp_ids.size, wl.restrict_ids.size
+    fc = wl.faces
+    orient = fc.normal * 2 + fc.side
+    ord_i = wl.interp_ids[np.argsort(orient[wl.interp_ids], kind="stable")]
+    ord_r = wl.restrict_ids[np.argsort(orient[wl.restrict_ids], kind="stable")]
+    n_i, n_r = ord_i.size, ord_r.size
     per_i, per_r = 2 * k * p * p * u, 2 * k * 9 * p * p * u
-    h_i = torch.empty(n_i * per_i, dtype=torch.float64, pin_memory=True)
+    tgt = k * p * p * u
+    # host copies of the per-face reference source buffers, in orientation order
+    h_i = torch.empty(max(1, n_i * per_i), dtype=torch.float64, pin_memory=True)
     for a in range(0, n_i, 1024):
         b = min(n_i, a + 1024)
-        h_i[a * per_i:b * per_i].copy_(W.interp_source_boxes(wl, wl.interp_ids[a:b]).reshape(-1))
+        h_i[a * per_i:b * per_i].copy_(W.interp_source_boxes(wl, ord_i[a:b]).reshape(-1))
     h_r = torch.empty(max(1, n_r * per_r), dtype=torch.float64, pin_memory=True)
     if n_r:
-        h_r.copy_(wl.fine)
+        pos = {f: j for j, f in enumerate(wl.restrict_ids)}
+        fine = wl.fine.view(n_r, per_r)
+        for a in range(0, n_r, 512):
+            b = min(n_r, a + 512)
+            idx = torch.as_tensor([pos[f] for f in ord_r[a:b]], device=fine.device)
+            h_r[a * per_r:b * per_r].copy_(fine.index_select(0, idx).reshape(-1))
     d_i = torch.empty(max(1, n_i * per_i), dtype=torch.float64, device=dev)
     d_r = torch.empty(max(1, n_r * per_r), dtype=torch.float64, device=dev)
-    n_chunks = 8
-    chunks = []
-    outs_h = []
-    fc = wl.faces
+    # normal layers each role's operators read (union over the passes)
+    layers = {}
     for ps in passes:
-        outs_h.append(torch.empty(ps["out"].numel(), dtype=torch.float64, pin_memory=True))
+        lo, cnt = ps["batch"].op.support_layers()
+        a, b = layers.get(ps["role"], (lo, lo + cnt))
+        layers[ps["role"]] = (min(a, lo), max(b, lo + cnt))
+    n_chunks = 8
+    outs_d = [torch.empty(ps["out"].numel(), dtype=torch.float64, device=dev) for ps in passes]
+    outs_h = [torch.empty(ps["out"].numel(), dtype=torch.float64, pin_memory=True) for ps in passes]
+    chunks = []
+    h2d = 0
     for c in range(n_chunks):
         ia, ib = n_i * c // n_chunks, n_i * (c + 1) // n_chunks
         ra, rb = n_r * c // n_chunks, n_r * (c + 1) // n_chunks
+        copies = []
+        for role, order, a0, b0, per, host, devb, t_ext in (
+                ("interpolate", ord_i, ia, ib, per_i, h_i, d_i, p), ("restrict", ord_r, ra, rb, per_r, h_r, d_r, 3 * p)):
+            if role not in layers or b0 <= a0:
+                continue
+            lo, hi = layers[role]
+            o = orient[order[a0:b0]]
+            cuts = np.flatnonzero(np.diff(o)) + 1
+            for g0, g1 in zip(np.r_[0, cuts], np.r_[cuts, o.size]):
+                nrm, side = int(o[g0]) // 2, int(o[g0]) % 2
+                wlo = lo if side == 0 else 2 * k - hi
+                off = (a0 + g0) * per * 8
+                copies.append((host.data_ptr() + off, devb.data_ptr() + off, int(g1 - g0), nrm, 2 * k, t_ext, wlo,
+                               hi - lo))
+                h2d += int(g1 - g0) * (hi - lo) * t_ext * t_ext * u * 8
         batches = []
         for ps in passes:
             op = ps["batch"].op
             if ps["role"] == "interpolate":
-                ids = wl.interp_ids[ia:ib]
+                ids = ord_i[ia:ib]
                 rec = th.slab_faces("interpolate", p, k, u, fc.normal[ids], fc.side[ids], segments=fc.segment[ids],
-                                    src_offsets=np.arange(ia, ib) * per_i,
-                                    dst_offsets=np.arange(ia, ib) * k * p * p * u)
-                lo, hi = ia, ib
+                                    src_offsets=np.arange(ia, ib) * per_i, dst_offsets=np.arange(ia, ib) * tgt)
+                lo_, hi_ = ia, ib
             else:
-                ids = wl.restrict_ids[ra:rb]
+                ids = ord_r[ra:rb]
                 rec = th.slab_faces("restrict", p, k, u, fc.normal[ids], fc.side[ids],
-                                    src_offsets=np.arange(ra, rb) * per_r,
-                                    dst_offsets=np.arange(ra, rb) * k * p * p * u)
-                lo, hi = ra, rb
-            batches.append((th.FaceBatch(op, rec, u) if hi > lo else None, lo, hi))
-        chunks.append(dict(ia=ia, ib=ib, ra=ra, rb=rb, batches=batches))
+                                    src_offsets=np.arange(ra, rb) * per_r, dst_offsets=np.arange(ra, rb) * tgt)
+                lo_, hi_ = ra, rb
+            batches.append((th.FaceBatch(op, rec, u) if hi_ > lo_ else None, lo_, hi_))
+        chunks.append(dict(copies=copies, batches=batches))
     s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    tgt = k * p * p * u
 
     def e2e_step():
         for ch in chunks:
-            with torch.cuda.stream(s_in):
-                if ch["ib"] > ch["ia"]:
-                    d_i[ch["ia"] * per_i:ch["ib"] * per_i].copy_(h_i[ch["ia"] * per_i:ch["ib"] * per_i], non_blocking=True)
-                if ch["rb"] > ch["ra"]:
-                    d_r[ch["ra"] * per_r:ch["rb"] * per_r].copy_(h_r[ch["ra"] * per_r:ch["rb"] * per_r], non_blocking=True)
-                e_in = torch.cuda.Event()
-                e_in.record(s_in)
+            for (hs, ds, n, nrm, n_ext, t_ext, wlo, cnt) in ch["copies"]:
+                _native.check(lib.th_copy_box_layers(hs, ds, n, nrm, n_ext, t_ext, u, wlo, cnt, 0, s_in.cuda_stream))
+            e_in = torch.cuda.Event()
+            e_in.record(s_in)
             s_run.wait_event(e_in)
             with torch.cuda.stream(s_run):
-                for ps, (batch, lo, hi) in zip(passes, ch["batches"]):
+                for ps, od, (batch, lo_, hi_) in zip(passes, outs_d, ch["batches"]):
                     if batch is not None:
-                        batch.launch(d_i if ps["role"] == "interpolate" else d_r, ps["out"], check_flag=False)
+                        batch.launch(d_i if ps["role"] == "interpolate" else d_r, od, check_flag=False)
                 e_run = torch.cuda.Event()
                 e_run.record(s_run)
             s_out.wait_event(e_run)
             with torch.cuda.stream(s_out):
-                for ps, oh, (batch, lo, hi) in zip(passes, outs_h, ch["batches"]):
-                    if hi > lo:
-                        oh[lo * tgt:hi * tgt].copy_(ps["out"][lo * tgt:hi * tgt], non_blocking=True)
+                for od, oh, (batch, lo_, hi_) in zip(outs_d, outs_h, ch["batches"]):
+                    if hi_ > lo_:
+                        oh[lo_ * tgt:hi_ * tgt].copy_(od[lo_ * tgt:hi_ * tgt], non_blocking=True)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -450,13 +481,23 @@ def run_e2e(args, wl, passes, dev, world):
         tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_step = float(tt.item())
+    # the e2e results must equal the device-resident run's (same faces, orientation order)
+    agree = True
+    for ps, oh in zip(passes, outs_h):
+        order = ord_i if ps["role"] == "interpolate" else ord_r
+        ids = wl.interp_ids if ps["role"] == "interpolate" else wl.restrict_ids
+        pos = {f: j for j, f in enumerate(ids)}
+        j = np.array([pos[f] for f in order[:64]])
+        ref = ps["out"].view(-1, tgt)[torch.as_tensor(j, device=ps["out"].device)].cpu()
+        agree &= bool(torch.equal(ref.reshape(-1), oh[: 64 * tgt]))
     values = sum(ps["values"] for ps in passes) * world
     return {"value": values / t_step, "unit": "values/s",
-            "h2d_bytes_per_step": int((n_i * per_i + n_r * per_r) * 8),
-            "d2h_bytes_per_step": int(sum(ps["out"].numel() for ps in passes) * 8),
-            "ms_per_step": round(t_step * 1e3, 2),
-            "how": "pinned host buffers of the per-face reference source layouts -> th_apply_faces -> pinned host "
-                   "outputs, 8 chunks pipelined over copy/compute/copy streams; wall clock with device sync"}
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(sum(ps["out"].numel() for ps in passes) * 8),
+            "ms_per_step": round(t_step * 1e3, 2), "matches_device_run": agree,
+            "how": "pinned host buffers of the per-face reference source layouts -> only the operators' normal "
+                   "support layers shipped (th_copy_box_layers, strided 2D/3D async copies) -> th_apply_faces -> "
+                   "pinned host outputs; 8 chunks pipelined over copy/compute/copy streams; wall clock with "
+                   "device sync"}
 
 
 def cpu_threads():

@@ -146,6 +146,20 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
  * otherwise (the whole-source check of schemes.py:186 / csr.py:165). */
 int32_t th_check_finite(const double* values, int64_t n, int32_t* flag, void* stream);
 
+/* Normal source layers an operator reads, in reference order [lo, lo + count)
+ * of the 2k source layers (the union of its stencil windows).  World layers are
+ * the same for coarse side 0 and mirrored (2k - lo - count) for side 1. */
+int32_t th_operator_support_layers(const th_operator* op, int32_t* lo, int32_t* count);
+
+/* Asynchronous copy of n_faces back-to-back world boxes (x fastest, u unknowns
+ * per cell, extent n_ext along `normal`, t_ext along the two tangential axes)
+ * restricted to the normal layers [lo, lo + count): one cudaMemcpy2DAsync /
+ * cudaMemcpy3DAsync for the whole group.  kind: 0 host->device, 1 device->host
+ * (host memory should be pinned).  Used to ship only an operator's support
+ * from host buffers in the reference layout. */
+int32_t th_copy_box_layers(const double* src, double* dst, int64_t n_faces, int32_t normal, int32_t n_ext,
+                           int32_t t_ext, int32_t u, int32_t lo, int32_t count, int32_t kind, void* stream);
+
 /* CSR apply on reference-frame AoS buffers (csr.py:143-173); all pointers device. */
 int32_t th_csr_apply(const int64_t* row_offsets, const int64_t* col_indices, const double* values,
                      int64_t n_rows, const double* src, double* out, int32_t u, void* stream);

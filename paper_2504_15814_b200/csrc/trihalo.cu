@@ -689,6 +689,51 @@ int32_t th_check_finite(const double* values, int64_t n, int32_t* flag, void* st
   return TH_OK;
 }
 
+int32_t th_operator_support_layers(const th_operator* op, int32_t* lo, int32_t* count) {
+  if (!op || !lo || !count) return fail(TH_ERR_CONFIG, "NULL argument");
+  int a = op->host.ax[0].ns, b = 0;
+  for (const auto& g : op->host.groups[0]) {
+    a = std::min(a, g.win0);
+    b = std::max(b, g.win0 + g.winL);
+  }
+  *lo = a;
+  *count = b - a;
+  return TH_OK;
+}
+
+int32_t th_copy_box_layers(const double* src, double* dst, int64_t n_faces, int32_t normal, int32_t n_ext,
+                           int32_t t_ext, int32_t u, int32_t lo, int32_t count, int32_t kind, void* stream) {
+  if (n_faces <= 0 || count <= 0) return TH_OK;
+  if (!src || !dst) return fail(TH_ERR_CONTRACT, "NULL pointer");
+  if (normal < 0 || normal > 2 || lo < 0 || lo + count > n_ext || u < 1 || t_ext < 1)
+    return fail(TH_ERR_CONFIG, "bad box layer selection");
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t cell = size_t(u) * sizeof(double);
+  const size_t box = cell * size_t(n_ext) * t_ext * t_ext;
+  if (normal == 2) {  // z slowest: the layers are one contiguous run per face
+    const size_t plane = cell * size_t(t_ext) * t_ext;
+    TH_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(dst) + lo * plane, box,
+                              reinterpret_cast<const char*>(src) + lo * plane, box, count * plane, size_t(n_faces), k, s));
+    return TH_OK;
+  }
+  // normal y: per face, t_ext z-planes each holding `count` contiguous rows of t_ext cells;
+  // normal x: per face, t_ext^2 rows of n_ext cells of which `count` are taken
+  const size_t row = normal == 1 ? cell * t_ext * n_ext : cell * n_ext;       // pitch between runs
+  const size_t width = normal == 1 ? cell * t_ext * count : cell * count;     // bytes per run
+  const size_t runs = normal == 1 ? size_t(t_ext) : size_t(t_ext) * t_ext;    // runs per face
+  const size_t off = normal == 1 ? cell * t_ext * lo : cell * lo;
+  cudaMemcpy3DParms prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.srcPtr = make_cudaPitchedPtr(const_cast<char*>(reinterpret_cast<const char*>(src)) + off, row, row, runs);
+  prm.dstPtr = make_cudaPitchedPtr(reinterpret_cast<char*>(dst) + off, row, row, runs);
+  prm.extent = make_cudaExtent(width, runs, size_t(n_faces));
+  prm.kind = k;
+  (void)box;
+  TH_CUDA(cudaMemcpy3DAsync(&prm, s));
+  return TH_OK;
+}
+
 int32_t th_csr_apply(const int64_t* row_offsets, const int64_t* col_indices, const double* values, int64_t n_rows,
                      const double* src, double* out, int32_t u, void* stream) {
   if (u < 1) return fail(TH_ERR_CONFIG, "u must be >= 1");

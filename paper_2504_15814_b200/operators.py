@@ -106,6 +106,12 @@ class HostOperator:
                 pass
             self.handle = None
 
+    def support_layers(self) -> tuple:
+        """Reference normal source layers [lo, lo + count) the operator reads."""
+        lo, cnt = ctypes.c_int32(), ctypes.c_int32()
+        _native.check(_native.load().th_operator_support_layers(self.handle, ctypes.byref(lo), ctypes.byref(cnt)))
+        return lo.value, cnt.value
+
     @property
     def max_condition(self) -> float:
         return float(self.info.max_condition)
