@@ -220,6 +220,14 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": args.steps * len(passes),
         "clocks": clocks,
     }
+    # measured DRAM traffic of the dominant kernel (ncu --set full, committed under profiles/)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"config{s.config}", {})
+        result["roofline"]["traffic"] = tr.get(f"{passes[dom]['role']}:{passes[dom]['scheme']}")
+        result["roofline"]["traffic_source"] = "profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum)"
+    except (OSError, ValueError):
+        pass
     step_bytes = sum(ps["bytes"] for ps in passes)
     result["step_alg_GBps"] = round(step_bytes / (ms_per_step / 1e3) / 1e9, 1)
     result["step_frac_hbm"] = round(step_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4)
