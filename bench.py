@@ -433,9 +433,9 @@ def run_e2e(args, wl, passes, dev, world):
             for g0, g1 in zip(np.r_[0, cuts], np.r_[cuts, o.size]):
                 nrm, side = int(o[g0]) // 2, int(o[g0]) % 2
                 wlo = lo if side == 0 else 2 * k - hi
-                off = (a0 + g0) * per * 8
-                copies.append((host.data_ptr() + off, devb.data_ptr() + off, int(g1 - g0), nrm, 2 * k, t_ext, wlo,
-                               hi - lo))
+                off = int(a0 + g0) * per * 8
+                copies.append((int(host.data_ptr() + off), int(devb.data_ptr() + off), int(g1 - g0), nrm, 2 * k,
+                               t_ext, int(wlo), int(hi - lo)))
                 h2d += int(g1 - g0) * (hi - lo) * t_ext * t_ext * u * 8
         batches = []
         for ps in passes:
