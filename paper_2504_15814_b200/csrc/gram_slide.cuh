@@ -19,16 +19,20 @@
 // shared memory; a block then only does its z-pass and synthesis.
 #pragma once
 
-template <int ORDER, int ROLE, int MINB>
+// TENSOR = true runs tensor_linear through the same slice ring: the x / y / z
+// passes apply the d-linear 1-D rows (normal, t1, t2 — the reference's
+// contraction order, linear.py:115-151) instead of Gram projections, with
+// ORDER = 2 standing for the 3-cell windows.
+template <int ORDER, int ROLE, int MINB, bool TENSOR = false>
 __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const double* __restrict__ src,
                                                                double* __restrict__ dst,
                                                                const th_face* __restrict__ faces, int64_t n_faces,
                                                                int u, int32_t* flag) {
   constexpr int L = ORDER == 2 ? 3 : 5;
   constexpr int D = ORDER + 1;
-  constexpr int NT = ORDER == 2 ? 6 : 10;   // pairs a + b <= ORDER
-  constexpr int NM = ORDER == 2 ? 10 : 20;  // triples a + b + c <= ORDER
   constexpr int C0 = 3, CT = ROLE == 0 ? 3 : 1;
+  constexpr int NT = TENSOR ? C0 * CT : (ORDER == 2 ? 6 : 10);  // per-slice values: pairs a + b <= ORDER
+  constexpr int NM = ORDER == 2 ? 10 : 20;                      // triples a + b + c <= ORDER
   extern __shared__ double ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* const ring = ring_all + warp * (L * NT * 32) + lane;  // [slot][t] x 32 lanes, lane-private
@@ -76,6 +80,19 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
     }
     const double* s0 = op.synth0 + g0 * 12;
     const double* s1 = op.synth1 + g1 * 12;
+    double R0[TENSOR ? C0 : 1][TENSOR ? L : 1], R1[TENSOR ? CT : 1][TENSOR ? L : 1];
+    if constexpr (TENSOR) {
+      const double* r0 = op.rows0 + __ldg(&op.row_off0[g0]);
+      const double* r1 = op.rows1 + __ldg(&op.row_off1[g1]);
+#pragma unroll
+      for (int c = 0; c < C0; ++c)
+#pragma unroll
+        for (int x = 0; x < L; ++x) R0[c][x] = c < G0.w ? __ldg(r0 + c * L + x) : 0.0;
+#pragma unroll
+      for (int c = 0; c < CT; ++c)
+#pragma unroll
+        for (int y = 0; y < L; ++y) R1[c][y] = c < G1.w ? __ldg(r1 + c * L + y) : 0.0;
+    }
     int hi = -1;  // highest t2 source slice held in the ring
     for (int g2 = fr.g2; g2 < fr.g2 + fr.n2; ++g2) {
       const int4 G2 = __ldg(&op.grp1[g2]);
@@ -86,7 +103,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         const int b2 = ROLE == 0 ? 0 : (a2 >= p) + (a2 >= 2 * p);
         const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
         // L2 bulk prefetch of the next slice (one cell per lane) while this one is projected
-        if (op.prefetch && lane < L * L && a2 + 1 < op.ns_t) {
+        if ((op.prefetch & 2) && lane < L * L && a2 + 1 < op.ns_t) {
           const int x = lane % L, y = lane / L, an = a2 + 1;
           const int bn = ROLE == 0 ? 0 : (an >= p) + (an >= 2 * p);
           const int64_t e = ybase[y] - (cb + lane) + int64_t(an - bn * p) * fr.s2 + int64_t(x) * fr.sn +
@@ -105,18 +122,29 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         for (int t = 0; t < NT; ++t) T[t] = 0.0;
 #pragma unroll
         for (int y = 0; y < L; ++y) {
-          double m[D];
+          if constexpr (TENSOR) {
 #pragma unroll
-          for (int a = 0; a < D; ++a) {
-            m[a] = 0.0;
+            for (int c0 = 0; c0 < C0; ++c0) {
+              double tx = 0.0;
 #pragma unroll
-            for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[y][x]);
+              for (int x = 0; x < L; ++x) tx = fma(R0[c0][x], v[y][x], tx);
+#pragma unroll
+              for (int c1 = 0; c1 < CT; ++c1) T[c0 + C0 * c1] = fma(R1[c1][y], tx, T[c0 + C0 * c1]);
+            }
+          } else {
+            double m[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              m[a] = 0.0;
+#pragma unroll
+              for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[y][x]);
+            }
+            int t = 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+              for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
           }
-          int t = 0;
-#pragma unroll
-          for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
         }
         double* slot = ring + (a2 % L) * (NT * 32);
 #pragma unroll
@@ -124,6 +152,40 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         asm volatile("" ::: "memory");  // one slice of loads live at a time
       }
       hi = max(hi, w2 + L - 1);
+      if constexpr (TENSOR) {
+        // ---- z-pass with the t2 rows straight into the children, store --------
+        const double* r2 = op.rows1 + __ldg(&op.row_off1[g2]);
+        const int slot0 = w2 % L;
+        bool bad = false;
+        double* const dbase = dst + fr.dst + cb + lane;
+#pragma unroll
+        for (int l = 0; l < CT; ++l) {
+          const int tz = G2.z + l;
+          if (!(l < G2.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
+          const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
+          double o[NT];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) o[t] = 0.0;
+#pragma unroll
+          for (int z = 0; z < L; ++z) {
+            const double w = ldg_slice(r2 + l * L + z);
+            const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
+            const double* slot = ring + sl * (NT * 32);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) o[t] = fma(w, slot[t * 32], o[t]);
+          }
+#pragma unroll
+          for (int j = 0; j < CT; ++j)
+#pragma unroll
+            for (int i = 0; i < C0; ++i)
+              if (ok1[j] && ok0[i] && ok) {
+                dbase[do0[i] + do1[j] + do2] = o[i + C0 * j];
+                bad |= !isfinite(o[i + C0 * j]);
+              }
+        }
+        raise_flag(flag, bad);
+        continue;
+      }
       // ---- z-pass of this block -------------------------------------------------
       double M[NM];
 #pragma unroll

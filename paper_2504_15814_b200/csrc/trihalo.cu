@@ -633,7 +633,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   // (bit 1: interpolation, bit 2: order3 restriction)
   // (bit 4: order3 restriction through the asynchronous slice pipeline, gram_restrict.cuh)
   //  experimental, off by default: measured 0.30 vs 0.37 of HBM for bit 2 on config 3)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 3; }();
+  //  bit 8: tensor_linear interpolation through the slice ring)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 11; }();
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
