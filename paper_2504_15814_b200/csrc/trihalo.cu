@@ -636,7 +636,15 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   //  bit 8: tensor_linear interpolation through the slice ring)
   static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 11; }();
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
-  if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
+  if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
+    // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
+    auto kfn = gram_slide_kernel<2, 0, 4, true>;
+    const size_t smem = size_t(4) * 3 * 9 * 32 * 8;
+    const int64_t units = n_faces * int64_t(op->dev.units_per_face) * ((u + 31) / 32);
+    const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 8));
+    kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  }
+  else if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
   else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->r_mode == 1 && op->r_L == 5 && h.p >= 4) {
     // one normal group of 3 children, 1-child tangential groups (checked by prepare_restrict);
