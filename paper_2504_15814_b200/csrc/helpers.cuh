@@ -30,3 +30,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
+
+// L2 prefetch of one AoS cell through the LSU (one prefetch.global.L2 per 128-byte
+// line, spread over lanes by the caller); unlike the TMA bulk prefetch it does not
+// queue behind the tensor-memory engine
+__device__ __forceinline__ void l2_prefetch_line(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}

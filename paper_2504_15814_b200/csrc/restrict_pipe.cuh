@@ -97,6 +97,21 @@ __global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
           const int a2 = G2.x + z;
           const int b2 = (a2 >= p) + (a2 >= 2 * p);
           const int64_t zo = int64_t(a2 - b2 * p) * fr.s2 + adj + cb;
+          if (L == 5 && (op.prefetch & 4) && z + 1 < L) {
+            // per-line L2 prefetch of slice z+1 (25 cells x 4 lines over the 32 lanes)
+            const int a2n = a2 + 1, b2n = (a2n >= p) + (a2n >= 2 * p);
+            const int64_t zon = int64_t(a2n - b2n * p) * fr.s2 + adj - lane;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int line = lane + 32 * r;
+              if (line < L * L * 4) {
+                const int cell = line >> 2, part = line & 3;
+                const int x = cell % L, y = cell / L;
+                const double* g = src + (__ldg(&fp->src[yb[y] + 3 * b2n]) + yo[y] + zon + int64_t(x) * fr.sn) + part * 16;
+                l2_prefetch_line(g);
+              }
+            }
+          }
           double v[L][L][NU];
 #pragma unroll
           for (int y = 0; y < L; ++y) {
