@@ -620,6 +620,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   } while (0)
   // TH_RESTRICT_NU=1 selects the one-unknown-per-lane variant (tuning experiments)
   static const int rnu = [] { const char* e = std::getenv("TH_RESTRICT_NU"); return e && e[0] == '1' ? 1 : 2; }();
+  static const int rminb = [] { const char* e = std::getenv("TH_RMINB"); return e ? std::atoi(e) : 5; }();
 #define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
   do {                                                                                                 \
     auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
@@ -659,6 +660,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   }
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
 #undef TH_GRAM
+  else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(1, 3, 1, 2, 6, 12);
+  else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(2, 3, 1, 2, 6, 12);
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
   else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 1, 6, 12);
   else if (op->r_mode == 1 && op->r_L == 5 && rnu == 2) TH_RREG(1, 5, 9, 2, 4, 8);
