@@ -621,6 +621,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   // TH_RESTRICT_NU=1 selects the one-unknown-per-lane variant (tuning experiments)
   static const int rnu = [] { const char* e = std::getenv("TH_RESTRICT_NU"); return e && e[0] == '1' ? 1 : 2; }();
   static const int rminb = [] { const char* e = std::getenv("TH_RMINB"); return e ? std::atoi(e) : 5; }();
+  static const int gminb = [] { const char* e = std::getenv("TH_GMINB"); return e ? std::atoi(e) : 4; }();
 #define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
   do {                                                                                                 \
     auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
@@ -658,6 +659,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 2));
     kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
   }
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 3) TH_GRAM(3, 1, 3);
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 5) TH_GRAM(3, 1, 5);
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
 #undef TH_GRAM
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(1, 3, 1, 2, 6, 12);
