@@ -621,7 +621,10 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   // TH_RESTRICT_NU=1 selects the one-unknown-per-lane variant (tuning experiments)
   static const int rnu = [] { const char* e = std::getenv("TH_RESTRICT_NU"); return e && e[0] == '1' ? 1 : 2; }();
   static const int rminb = [] { const char* e = std::getenv("TH_RMINB"); return e ? std::atoi(e) : 5; }();
-  static const int gminb = [] { const char* e = std::getenv("TH_GMINB"); return e ? std::atoi(e) : 4; }();
+  static const int gminb = [] { const char* e = std::getenv("TH_GMINB"); return e ? std::atoi(e) : 3; }();
+  // register budgets chosen so that no hot kernel spills (spills measured 25-35% slower);
+  // TH_MINBSET=0 restores the earlier, tighter budgets for A/B runs
+  static const int minbset = [] { const char* e = std::getenv("TH_MINBSET"); return e ? std::atoi(e) : 1; }();
 #define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
   do {                                                                                                 \
     auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
@@ -640,12 +643,13 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
     // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
-    auto kfn = gram_slide_kernel<2, 0, 4, true>;
+    auto kfn = minbset ? gram_slide_kernel<2, 0, 3, true> : gram_slide_kernel<2, 0, 4, true>;
     const size_t smem = size_t(4) * 3 * 9 * 32 * 8;
     const int64_t units = n_faces * int64_t(op->dev.units_per_face) * ((u + 31) / 32);
     const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 8));
     kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
   }
+  else if (gram && interp && h.scheme == 2 && minbset) TH_GRAM(2, 0, 4);
   else if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
   else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->r_mode == 1 && op->r_L == 5 && h.p >= 4) {
@@ -665,6 +669,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
 #undef TH_GRAM
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(1, 3, 1, 2, 6, 12);
   else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(2, 3, 1, 2, 6, 12);
+  else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && minbset) TH_RREG(1, 3, 1, 2, 4, 8);
+  else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2 && minbset) TH_RREG(2, 3, 1, 2, 4, 8);
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
   else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 1, 6, 12);
   else if (op->r_mode == 1 && op->r_L == 5 && rnu == 2) TH_RREG(1, 5, 9, 2, 4, 8);
