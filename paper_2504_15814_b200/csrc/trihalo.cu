@@ -625,6 +625,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   // register budgets chosen so that no hot kernel spills (spills measured 25-35% slower);
   // TH_MINBSET=0 restores the earlier, tighter budgets for A/B runs
   static const int minbset = [] { const char* e = std::getenv("TH_MINBSET"); return e ? std::atoi(e) : 1; }();
+  static const int imin = [] { const char* e = std::getenv("TH_IMINB"); return e ? std::atoi(e) : 0; }();  // A/B
 #define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
   do {                                                                                                 \
     auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
@@ -643,12 +644,14 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
     // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
-    auto kfn = minbset ? gram_slide_kernel<2, 0, 3, true> : gram_slide_kernel<2, 0, 4, true>;
+    auto kfn = imin == 5 ? gram_slide_kernel<2, 0, 5, true> : gram_slide_kernel<2, 0, 4, true>;
     const size_t smem = size_t(4) * 3 * 9 * 32 * 8;
     const int64_t units = n_faces * int64_t(op->dev.units_per_face) * ((u + 31) / 32);
     const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 8));
     kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
   }
+  else if (gram && interp && h.scheme == 2 && imin == 3) TH_GRAM(2, 0, 3);
+  else if (gram && interp && h.scheme == 3 && imin == 2) TH_GRAM(3, 0, 2);
   else if (gram && interp && h.scheme == 2 && minbset) TH_GRAM(2, 0, 4);
   else if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
