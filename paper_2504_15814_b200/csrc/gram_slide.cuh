@@ -102,22 +102,8 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
       for (int a2 = max(hi + 1, w2); a2 < w2 + L; ++a2) {
         const int b2 = ROLE == 0 ? 0 : (a2 >= p) + (a2 >= 2 * p);
         const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
-        // L2 bulk prefetch of the next slice (one cell per lane) while this one is projected
-        if ((op.prefetch & 2) && a2 + 1 < op.ns_t) {
-          // per-line L2 prefetch of the next slice (L*L cells x 4 lines over the lanes)
-          const int an = a2 + 1;
-          const int bn = ROLE == 0 ? 0 : (an >= p) + (an >= 2 * p);
-#pragma unroll
-          for (int r = 0; r < (L * L * 4 + 31) / 32; ++r) {
-            const int line = lane + 32 * r;
-            if (line < L * L * 4) {
-              const int cell = line >> 2, part = line & 3, x = cell % L, y = cell / L;
-              const int64_t e = ybase[y] - (cb + lane) + int64_t(an - bn * p) * fr.s2 + int64_t(x) * fr.sn +
-                                (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * bn])) + part * 16;
-              l2_prefetch_line(src + e);
-            }
-          }
-        }
+        // (no prefetch of the next slice: TMA bulk and per-line L2 prefetches both measured
+        //  slower here, and indexing ybase[] at run time would push it to local memory)
         double v[L][L];
 #pragma unroll
         for (int y = 0; y < L; ++y) {
