@@ -55,13 +55,14 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
     const bool ok = cb + lane < u;
     // source line bases per t1 row y (restriction adds the fine block of (y, z))
     const int64_t adj = ROLE == 0 ? 0 : fr.src0 - __ldg(&fp->src[0]);
-    int64_t ybase[L];
-    int yb[L];
+    const int64_t ibase = fr.src0 + int64_t(G1.x) * fr.s1 + int64_t(G0.x) * fr.sn + cb + lane;
+    int64_t ybase[ROLE == 0 ? 1 : L];
+    int yb[ROLE == 0 ? 1 : L];
 #pragma unroll
-    for (int y = 0; y < L; ++y) {
+    for (int y = 0; y < (ROLE == 0 ? 1 : L); ++y) {
       const int a1 = G1.x + y;
       yb[y] = ROLE == 0 ? 0 : (a1 >= p) + (a1 >= 2 * p);
-      ybase[y] = (ROLE == 0 ? fr.src0 : adj) + int64_t(a1 - yb[y] * p) * fr.s1 + int64_t(G0.x) * fr.sn + cb + lane;
+      ybase[y] = adj + int64_t(a1 - yb[y] * p) * fr.s1 + int64_t(G0.x) * fr.sn + cb + lane;
     }
     // target offsets of the normal and t1 children
     int64_t do0[C0], do1[CT];
@@ -107,7 +108,10 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         double v[L][L];
 #pragma unroll
         for (int y = 0; y < L; ++y) {
-          const int64_t base = ybase[y] + zo + (ROLE == 0 ? 0 : __ldg(&fp->src[yb[y] + 3 * b2]));
+          // interpolation rows are affine in y (one base + y * s1, fewer live registers);
+          // restriction rows may cross a fine-block boundary, so they use the per-row table
+          const int64_t base = ROLE == 0 ? ibase + zo + int64_t(y) * fr.s1
+                                         : ybase[y] + zo + __ldg(&fp->src[yb[y] + 3 * b2]);
 #pragma unroll
           for (int x = 0; x < L; ++x) v[y][x] = ok ? ldg_slice(src + base + int64_t(x) * fr.sn) : 0.0;
         }
