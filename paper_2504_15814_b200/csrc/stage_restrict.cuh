@@ -1,0 +1,417 @@
+// order3 restriction with CTA-level staging (included by trihalo.cu after
+// gram_slide.cuh).
+//
+// What it computes is the reference's least-squares restriction
+// (taylor.py:171-219 rows, linear.py apply order) in the Gram-separable form of
+// gram_slide.cuh.  For a restriction face the t2 windows (L = 5 fine slices)
+// step by 3 and overlap by <= 2, so a fine slice feeds at most two coarse
+// columns, and the z-pass and t2 synthesis fold into one 1-D row per degree:
+//   Q_ab(j) = sum_z K_{a+b}(j, z) T_ab(w_j + z),  K_d(j, z) = sum_{c <= 3-d} S2_j[c] P_c(z)
+//   out_i   = sum_a S0_i[a] sum_b S1[b] Q_ab
+// with T_ab the per-slice x/y Gram moments.  Each consumer warp keeps the two
+// open windows' Q (20 doubles) in registers: no moment ring.
+//
+// Why staging: the per-warp slide is latency-bound (one 25-cell slice in
+// flight per warp, 12-16 warps/SM: 0.58 of HBM).  Here one CTA owns a
+// (face, t1 tile) and a producer warp streams the tile's fine slices -- planes
+// of NX (normal) x NY (t1) cells -- into an NST-stage shared-memory ring with
+// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx), so a whole plane
+// per stage is in flight without registers, and the t1-overlapping windows of
+// the tile's consumer warps read it from shared memory instead of L2.
+//
+// Bulk copies need 16-byte alignment; unpadded cells (u = 59: 472 B) are only
+// 8-byte aligned, and one copy per cell is op-rate bound (2.0 TB/s measured,
+// tools/probe/probe_stage.cu).  So the producer copies contiguous RUNS of
+// cells, widened to 16-byte boundaries (<= 8 extra bytes per end, inside the
+// allocation's 16-byte granules):
+//   mode 0  |sn| == u : one run per t1 line along the normal (NX cells)
+//   mode 1  s1 == u   : one run per (normal position, fine block) along t1
+//   mode 2  otherwise : one copy per cell (correct, slow; not used by the
+//                       standard slab / pool layouts)
+// Cell (x, y) of a stage then sits at  BASE + y*YS + x*XS + e(x, y)  doubles,
+// e = the run's 8-byte shift plus the per-run slack, 6-bit fields of a per-line
+// word written by the producer.
+#pragma once
+
+namespace stage {
+
+constexpr int L = 5, D = 4, NT = 10;
+
+struct Tile {
+  int gA, gB, y0, ny;
+};
+
+__device__ __forceinline__ Tile tile_of(const DevOp& op, int ti, int ntiles) {
+  Tile t;
+  t.gA = ti * op.G1 / ntiles;
+  t.gB = (ti + 1) * op.G1 / ntiles;
+  t.y0 = __ldg(&op.grp1[t.gA]).x;
+  t.ny = __ldg(&op.grp1[t.gB - 1]).x + L - t.y0;
+  return t;
+}
+
+__device__ __forceinline__ int round_even(int v) { return (v + 1) & ~1; }
+
+}  // namespace stage
+
+template <int NCW, int NST, int NU>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+    stage_restrict3_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
+                           const th_face* __restrict__ faces, int64_t n_faces, int u, int32_t* flag, int stage_d,
+                           int ny_max) {
+  using namespace stage;
+  extern __shared__ __align__(128) double sm[];
+  double* const stages = sm;                                        // [NST][stage_d]
+  double* const ktab = sm + NST * stage_d;                          // [G1][L][D]
+  int* const hdr = reinterpret_cast<int*>(ktab + op.G1 * L * D);    // [NST][4]: XS, YS, BASE
+  unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);  // [NST][ny_max]
+  unsigned char* const shr = reinterpret_cast<unsigned char*>(eline + NST * ny_max);  // producer scratch
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p = op.p, G1 = op.G1;
+  const int nch = (u + 32 * NU - 1) / (32 * NU);
+  const int tg = min(G1, NCW / nch);
+  const int ntiles = (G1 + tg - 1) / tg;
+  const int64_t total = n_faces * ntiles;
+  const int a2lo = __ldg(&op.grp1[0]).x, a2hi = __ldg(&op.grp1[G1 - 1]).x + L;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], NCW);
+    }
+    mbar_fence_init();
+  }
+  // K_d(j, z): the t2 synthesis folded into the z-pass (child 0 of each 1-child group)
+  for (int i = threadIdx.x; i < G1 * L * D; i += blockDim.x) {
+    const int g = i / (L * D), z = (i / D) % L, d = i % D;
+    const double* S = op.synth1 + g * 12;
+    double k = 0.0;
+    for (int c = 0; c + d < D; ++c) k = fma(__ldg(S + c), Gram<5>::P(c, z), k);
+    ktab[i] = k;
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ===================== producer =====================
+    int s = 0;
+    unsigned ph = 0;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int64_t f = tile / ntiles;
+      const th_face* fp = faces + f;
+      FaceRef fr;
+      decode_face(fp, op, fr);
+      if (fr.n0 != 1) continue;
+      const Tile t = tile_of(op, int(tile - f * ntiles), ntiles);
+      const int4 G0 = __ldg(&op.grp0[fr.g0]);
+      const int nx = G0.y, x0 = G0.x;
+      const int64_t adj = fr.src0 - __ldg(&fp->src[0]);
+      const int mode = (fr.sn == u || fr.sn == -u) ? 0 : (fr.s1 == u ? 1 : 2);
+      const int bfirst = t.y0 / p, nseg = (t.y0 + t.ny - 1) / p - bfirst + 1;
+      const int nruns = mode == 0 ? t.ny : mode == 1 ? nx * nseg : nx * t.ny;
+      // per-mode strides (doubles); mode 1's XS = sum over segments of the run slots
+      int XS, YS, BASE = 0;
+      if (mode == 0) {
+        YS = round_even(nx * u + 2);
+        XS = fr.sn > 0 ? u : -u;
+        BASE = fr.sn > 0 ? 0 : (nx - 1) * u;
+      } else if (mode == 1) {
+        YS = u;
+        XS = 0;
+        for (int sg = 0; sg < nseg; ++sg) {
+          const int ys = max(t.y0, (bfirst + sg) * p), ye = min(t.y0 + t.ny, (bfirst + sg + 1) * p);
+          XS += round_even((ye - ys) * u + 2);
+        }
+      } else {
+        YS = round_even(u + 2);
+        XS = t.ny * YS;
+      }
+      // ---- per-tile run descriptors (modes 0 / 1: <= 2 runs and <= 2 lines per lane) ----
+      // run r = lane + 32 k starts at  block base(b1, b2) + roff + zo(a2)  and lands at
+      // stage + rdst; only the block base and zo change from slice to slice
+      const bool fast = mode != 2 && nruns <= 64 && t.ny <= 64;
+      int rb1[2], rdst[2];
+      int64_t roff[2];
+      unsigned rlen[2];
+      int lsg[2], leb[2];  // mode 1 lines y = lane + 32 k: segment, per-tile part of e
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = lane + 32 * k;
+        rb1[k] = 0, rdst[k] = 0, roff[k] = 0, rlen[k] = 0, lsg[k] = 0, leb[k] = 0;
+        if (!fast) continue;
+        if (r < nruns) {
+          int x, ya, n, d;
+          if (mode == 0) {
+            x = fr.sn > 0 ? 0 : nx - 1;
+            ya = t.y0 + r;
+            n = nx;
+            d = r * YS;
+          } else {
+            x = r / nseg;
+            const int sg = r - x * nseg;
+            ya = max(t.y0, (bfirst + sg) * p);
+            n = min(t.y0 + t.ny, (bfirst + sg + 1) * p) - ya;
+            int off = 0;
+            for (int q = 0; q < sg; ++q) {
+              const int ys = max(t.y0, (bfirst + q) * p), ye = min(t.y0 + t.ny, (bfirst + q + 1) * p);
+              off += round_even((ye - ys) * u + 2);
+            }
+            d = x * XS + off;
+          }
+          rb1[k] = ya / p;
+          roff[k] = int64_t(ya - rb1[k] * p) * fr.s1 + int64_t(x0 + x) * fr.sn + adj;
+          rdst[k] = d;
+          rlen[k] = unsigned(n) * unsigned(u) * 8u;
+        }
+        const int y = r;
+        if (mode == 1 && y < t.ny) {
+          const int sg = (t.y0 + y) / p - bfirst;
+          int off = 0;
+          for (int q = 0; q < sg; ++q) {
+            const int ys = max(t.y0, (bfirst + q) * p), ye = min(t.y0 + t.ny, (bfirst + q + 1) * p);
+            off += round_even((ye - ys) * u + 2);
+          }
+          lsg[k] = sg;
+          leb[k] = off - (max(t.y0, (bfirst + sg) * p) - t.y0) * u;
+        }
+      }
+      int64_t rbb[2] = {0, 0};
+      int b2prev = -1;
+      for (int a2 = a2lo; a2 < a2hi; ++a2) {
+        mbar_wait(&empty[s], ph ^ 1);
+        const int b2 = a2 / p;
+        const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
+        double* const st = stages + size_t(s) * stage_d;
+        if (fast) {
+          if (b2 != b2prev) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              if (lane + 32 * k < nruns) rbb[k] = __ldg(&fp->src[rb1[k] + 3 * b2]);
+            b2prev = b2;
+          }
+          uintptr_t lo[2];
+          unsigned nb[2], sh[2];
+          unsigned bytes = 0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const uintptr_t ga = reinterpret_cast<uintptr_t>(src + (rbb[k] + roff[k] + zo));
+            lo[k] = ga & ~uintptr_t(15);
+            nb[k] = unsigned(((ga + rlen[k] + 15) & ~uintptr_t(15)) - lo[k]);
+            sh[k] = unsigned(ga - lo[k]) >> 3;
+            if (lane + 32 * k < nruns) {
+              bytes += nb[k];
+              if (mode == 1) shr[lane + 32 * k] = (unsigned char)sh[k];
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+          if (lane == 0) {
+            mbar_expect_tx(&full[s], bytes);
+            int* h = hdr + s * 4;
+            h[0] = XS;
+            h[1] = YS;
+            h[2] = BASE;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            if (lane + 32 * k < nruns) bulk_g2s(st + rdst[k], reinterpret_cast<const void*>(lo[k]), nb[k], &full[s]);
+          // per-line shift words e(x, y), 6-bit fields
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int y = lane + 32 * k;
+            if (y >= t.ny) continue;
+            unsigned w;
+            if (mode == 0) {
+              w = sh[k] * 0x1041041u;  // the line's one run: same shift for every x
+            } else {
+              w = 0;
+              for (int x = 0; x < nx; ++x) w |= unsigned(leb[k] + shr[x * nseg + lsg[k]]) << (6 * x);
+            }
+            eline[s * ny_max + y] = w;
+          }
+        } else {
+          // mode 2 (no contiguous axis): one copy per cell, all recomputed per slice
+          const int64_t zoa = zo + adj;
+          unsigned bytes = 0;
+          for (int r = lane; r < nruns; r += 32) {
+            const int x = r / t.ny, ya = t.y0 + (r - x * t.ny), b1 = ya / p;
+            const uintptr_t ga = reinterpret_cast<uintptr_t>(
+                src + (__ldg(&fp->src[b1 + 3 * b2]) + int64_t(ya - b1 * p) * fr.s1 + zoa + int64_t(x0 + x) * fr.sn));
+            const uintptr_t lo = ga & ~uintptr_t(15);
+            bytes += unsigned(((ga + uintptr_t(u) * 8 + 15) & ~uintptr_t(15)) - lo);
+            shr[r] = (unsigned char)((ga - lo) >> 3);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+          if (lane == 0) {
+            mbar_expect_tx(&full[s], bytes);
+            int* h = hdr + s * 4;
+            h[0] = XS;
+            h[1] = YS;
+            h[2] = BASE;
+          }
+          __syncwarp();
+          for (int r = lane; r < nruns; r += 32) {
+            const int x = r / t.ny, ya = t.y0 + (r - x * t.ny), b1 = ya / p;
+            const uintptr_t ga = reinterpret_cast<uintptr_t>(
+                src + (__ldg(&fp->src[b1 + 3 * b2]) + int64_t(ya - b1 * p) * fr.s1 + zoa + int64_t(x0 + x) * fr.sn));
+            const uintptr_t lo = ga & ~uintptr_t(15);
+            bulk_g2s(st + x * XS + (ya - t.y0) * YS, reinterpret_cast<const void*>(lo),
+                     unsigned(((ga + uintptr_t(u) * 8 + 15) & ~uintptr_t(15)) - lo), &full[s]);
+          }
+          for (int y = lane; y < t.ny; y += 32) {
+            unsigned w = 0;
+            for (int x = 0; x < nx; ++x) w |= unsigned(shr[x * t.ny + y]) << (6 * x);
+            eline[s * ny_max + y] = w;
+          }
+        }
+        __syncwarp();  // shr reads above precede the next stage's writes
+        mbar_arrive(&full[s]);
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== consumers =====================
+    // warp w owns t1 group gA + w / nch and unknowns [cb, cb + 32 NU) of the tile;
+    // lane q-th unknown = cb + lane + 32 q
+    int s = 0;
+    unsigned ph = 0;
+    const int gi = warp / nch, chunk = warp - gi * nch;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int64_t f = tile / ntiles;
+      const th_face* fp = faces + f;
+      FaceRef fr;
+      decode_face(fp, op, fr);
+      if (fr.n0 != 1) continue;
+      const Tile t = tile_of(op, int(tile - f * ntiles), ntiles);
+      const bool active = gi < t.gB - t.gA && warp < tg * nch;
+      const int g1 = t.gA + (active ? gi : 0);
+      const int ly = __ldg(&op.grp1[g1]).x - t.y0;
+      const int cb = chunk * 32 * NU;
+      bool ok[NU];
+#pragma unroll
+      for (int q = 0; q < NU; ++q) ok[q] = active && cb + lane + 32 * q < u;
+      double QA[NU][NT], QB[NU][NT];
+#pragma unroll
+      for (int q = 0; q < NU; ++q)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) QA[q][i] = QB[q][i] = 0.0;
+      int j = 0;
+      int wA = __ldg(&op.grp1[0]).x;
+      int wB = G1 > 1 ? __ldg(&op.grp1[1]).x : INT_MAX / 2;
+      bool bad = false;
+      for (int a2 = a2lo; a2 < a2hi; ++a2) {
+        const int zA = a2 - wA, zB = a2 - wB;
+        const bool inA = zA >= 0 && zA < L, inB = zB >= 0 && zB < L;
+        mbar_wait(&full[s], ph);
+        if (active) {
+          const int* h = hdr + s * 4;
+          const int XS = h[0], YS = h[1], BASE = h[2];
+          const double* st = stages + size_t(s) * stage_d + BASE + cb + lane;
+          const unsigned* el = eline + s * ny_max + ly;
+          const double* kA = ktab + (j * L + (inA ? zA : 0)) * D;
+          const double* kB = ktab + ((j + 1) * L + (inB ? zB : 0)) * D;
+          // one unknown at a time: only one T[] live next to the open windows' Q
+#pragma unroll
+          for (int q = 0; q < NU; ++q) {
+            double T[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) T[i] = 0.0;
+#pragma unroll
+            for (int y = 0; y < L; ++y) {
+              const unsigned e = el[y];
+              const double* ln = st + (ly + y) * YS + 32 * q;
+              double v[L];
+#pragma unroll
+              for (int x = 0; x < L; ++x) v[x] = ok[q] ? ln[x * XS + int((e >> (6 * x)) & 63u)] : 0.0;
+              double m[D];
+#pragma unroll
+              for (int a = 0; a < D; ++a) {
+                m[a] = 0.0;
+#pragma unroll
+                for (int x = 0; x < L; ++x) gacc(m[a], Gram<5>::P(a, x), v[x]);
+              }
+              int tt = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) gacc(T[tt], Gram<5>::P(b, y), m[a]);
+            }
+            // z accumulation into the (at most two) open windows
+            if (inA) {
+              int tt = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) QA[q][tt] = fma(kA[a + b], T[tt], QA[q][tt]);
+            }
+            if (inB) {
+              int tt = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) QB[q][tt] = fma(kB[a + b], T[tt], QB[q][tt]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (!active) continue;
+        if (zA == L - 1) {
+          // ---- window j complete: synthesis at its children, store ----
+          const int t1 = __ldg(&op.grp1[g1]).z, t2 = __ldg(&op.grp1[j]).z;
+          if (t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p) {
+            const int4 G0 = __ldg(&op.grp0[fr.g0]);
+            const double* s1 = op.synth1 + g1 * 12;
+            const double* s0 = op.synth0 + fr.g0 * 12;
+            double* const ob = dst + fr.dst + int64_t(t1 - fr.lo1) * fr.d1 + int64_t(t2 - fr.lo2) * fr.d2 + cb + lane;
+#pragma unroll
+            for (int q = 0; q < NU; ++q) {
+              double R[D];
+              int tt = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a) {
+                R[a] = 0.0;
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + b), QA[q][tt], R[a]);
+              }
+#pragma unroll
+              for (int i = 0; i < 3; ++i) {
+                const int t0 = G0.z + i;
+                if (i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) {
+                  double o = 0.0;
+#pragma unroll
+                  for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
+                  if (ok[q]) {
+                    ob[int64_t(t0 - fr.lo0) * fr.dn + 32 * q] = o;
+                    bad |= !isfinite(o);
+                  }
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < NU; ++q)
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+              QA[q][i] = QB[q][i];
+              QB[q][i] = 0.0;
+            }
+          ++j;
+          wA = wB;
+          wB = j + 1 < G1 ? __ldg(&op.grp1[j + 1]).x : INT_MAX / 2;
+        }
+      }
+      if (active) raise_flag(flag, bad);
+    }
+  }
+}

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "window.cuh"
 #include "restrict_pipe.cuh"
 #include "gram_slide.cuh"
-#include "gram_restrict.cuh"
+#include "stage_restrict.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -374,6 +374,8 @@ struct th_operator {
   // restriction register kernel: mode (0 = not eligible), window, classes, params blob
   int r_mode = 0, r_L = 0, r_ncls = 0;
   std::vector<unsigned char> r_params;
+  // staged order3 restriction (stage_restrict.cuh) eligibility
+  bool st_ok = false;
 };
 
 namespace {
@@ -424,6 +426,60 @@ void prepare_restrict(th_operator* op) {
     op->r_mode = h.fast_mode;
     op->r_L = h.fast_L0;
   }
+}
+
+// eligibility of the staged order3 restriction (stage_restrict.cuh): every face
+// half has one normal group (5-cell window, <= 3 children); tangential groups
+// have 5-cell windows and one child, starts non-decreasing, and window j + 2
+// starts after window j ends (a fine slice feeds at most two coarse columns)
+void prepare_stage(th_operator* op) {
+  const th::HostOperator& h = op->host;
+  op->st_ok = false;
+  if (h.role != 1 || h.scheme != TH_SCHEME_ORDER3 || !h.gram_ok || h.synth[0].empty() || h.synth[1].empty()) return;
+  for (int a = 0; a < 3; ++a)
+    if (h.half_g[a][1] - h.half_g[a][0] > 1) return;
+  for (const auto& g : h.groups[0])
+    if (g.winL != 5 || g.tgtN < 1 || g.tgtN > 3) return;
+  const auto& g1 = h.groups[1];
+  if (g1.empty()) return;
+  for (size_t j = 0; j < g1.size(); ++j) {
+    if (g1[j].winL != 5 || g1[j].tgtN != 1) return;
+    if (j > 0 && g1[j].win0 < g1[j - 1].win0) return;
+    if (j + 2 < g1.size() && g1[j + 2].win0 < g1[j].win0 + 5) return;
+  }
+  op->st_ok = true;
+}
+
+// launch geometry of the staged restriction for u unknowns; false = does not fit
+struct StageGeom {
+  int nst = 0, stage_d = 0, ny_max = 0;
+  size_t smem = 0;
+};
+constexpr int kStageNCW = 9, kStageNU = 2;  // consumer warps per CTA (one per t1 group at u <= 64), unknowns per lane
+
+bool stage_geometry(const th_operator* op, int u, StageGeom& g) {
+  const th::HostOperator& h = op->host;
+  const int G1 = (int)h.groups[1].size();
+  const int nch = (u + 32 * kStageNU - 1) / (32 * kStageNU);
+  if (nch > kStageNCW) return false;
+  const int tg = std::min(G1, kStageNCW / nch);
+  const int ntiles = (G1 + tg - 1) / tg;
+  g.ny_max = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    const int gA = t * G1 / ntiles, gB = (t + 1) * G1 / ntiles;
+    g.ny_max = std::max(g.ny_max, h.groups[1][gB - 1].win0 + 5 - h.groups[1][gA].win0);
+  }
+  g.stage_d = (5 * g.ny_max * (u + 3) + 1) & ~1;
+  const size_t tail = size_t(G1) * 20 * 8 + 16 * 4 /*hdr*/ + size_t(4) * g.ny_max * 4 + size_t(5) * g.ny_max + 64;
+  for (int nst = 3; nst >= 2; --nst) {
+    const size_t smem = size_t(nst) * g.stage_d * 8 + tail;
+    if (smem <= 227 * 1024 - 1024) {
+      g.nst = nst;
+      g.smem = smem;
+      return true;
+    }
+  }
+  return false;
 }
 
 template <class T>
@@ -524,6 +580,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   op->smem_bytes = op->smem_ok ? size_t(d.n_blocks) * h.fast_L0 * h.fast_LT * h.fast_LT * 32 : 0;
   if (op->smem_bytes > 200 * 1024) op->smem_ok = false;
   prepare_restrict(op);
+  prepare_stage(op);
   if (!upload_to_device) {
     *out = op;
     return TH_OK;
@@ -637,10 +694,10 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   } while (0)
   // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
   // (bit 1: interpolation, bit 2: order3 restriction)
-  // (bit 4: order3 restriction through the asynchronous slice pipeline, gram_restrict.cuh)
-  //  experimental, off by default: measured 0.30 vs 0.37 of HBM for bit 2 on config 3)
+  // (bit 4: order3 restriction through the staged TMA kernel, stage_restrict.cuh;
   //  bit 8: tensor_linear interpolation through the slice ring)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 11; }();
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 15; }();
+  StageGeom sg;
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
   if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
     // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
@@ -655,16 +712,16 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   else if (gram && interp && h.scheme == 2 && minbset) TH_GRAM(2, 0, 4);
   else if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->r_mode == 1 && op->r_L == 5 && h.p >= 4) {
-    // one normal group of 3 children, 1-child tangential groups (checked by prepare_restrict);
-    // p >= 4 so that a fine slice feeds at most two coarse columns
-    constexpr int NST = 4;
-    auto kfn = gram_restrict3_kernel<NST, 2>;
-    const size_t smem = size_t(4) * NST * 25 * 32 * 8;
-    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int64_t units = n_faces * int64_t(op->dev.G1) * ((u + 31) / 32);
-    const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 2));
-    kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->st_ok && stage_geometry(op, u, sg)) {
+    // staged order3 restriction: persistent, one CTA per SM (stage_restrict.cuh)
+    auto kfn = sg.nst == 3 ? stage_restrict3_kernel<kStageNCW, 3, kStageNU> : stage_restrict3_kernel<kStageNCW, 2, kStageNU>;
+    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sg.smem)));
+    const int G1 = op->dev.G1, nch = (u + 32 * kStageNU - 1) / (32 * kStageNU);
+    const int tg = std::min(G1, kStageNCW / nch);
+    const int64_t tiles = n_faces * ((G1 + tg - 1) / tg);
+    const int sblocks = int(std::min<int64_t>(tiles, int64_t(num_sms())));
+    kfn<<<sblocks, (kStageNCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,
+                                                       sg.ny_max);
   }
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 3) TH_GRAM(3, 1, 3);
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 5) TH_GRAM(3, 1, 5);
