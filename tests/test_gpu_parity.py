@@ -268,3 +268,54 @@ def test_restrict_into_coarse_halo(th):
             ext[n] = hi_h - lo_h
             box = cp[f, lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]].reshape(-1)
             assert np.array_equal(box, slab[f])
+
+
+def _transpose_records(rec, E, u, patch, fields=("src",)):
+    """Re-address pool records for a z-fastest pool ([patch][x][y][z][u]); strides permuted."""
+    out = rec.copy()
+    for name in fields:
+        off = out[name].astype(np.int64)
+        pid, rem = np.divmod(off, patch)
+        cell, q = np.divmod(rem, u)
+        assert not q.any()
+        z, yx = np.divmod(cell, E * E)
+        y, x = np.divmod(yx, E)
+        out[name] = pid * patch + ((x * E + y) * E + z) * u
+    out["src_stride"] = [E * E * u, E * u, u]
+    return out
+
+
+@pytest.mark.parametrize("scheme", ("tensor_linear", "matrix_linear", "order2", "order3"))
+@pytest.mark.parametrize("p", (9, 17))
+def test_pool_transposed_layout(th, scheme, p):
+    """A z-fastest pool: x- and y-normal faces have no contiguous normal / t1 axis, so the
+    staged order3 restriction takes its one-copy-per-cell path (mode 2), z-normal faces
+    its normal-run path.  Results must equal the x-fastest run bit for bit."""
+    import torch
+
+    k, u = 3, 59
+    rng = np.random.default_rng(p + 31)
+    E = p + 2 * k
+    patch = E ** 3 * u
+    n_patch, n_face = 12, 24
+    pool = rng.standard_normal((n_patch, E, E, E, u))  # (z, y, x, u) per patch
+    pool_t = np.ascontiguousarray(pool.transpose(0, 3, 2, 1, 4))  # (x, y, z, u)
+    dev = torch.device("cuda")
+    src = torch.from_numpy(pool.reshape(-1)).to(dev)
+    src_t = torch.from_numpy(pool_t.reshape(-1)).to(dev)
+    nrm = np.arange(n_face) % 3
+    sid = (np.arange(n_face) // 3) % 2
+    cases = [("restrict", th.pool_restrict_faces(p, k, u, rng.integers(0, n_patch, (n_face, 9)), nrm, sid), k * p * p)]
+    if p == 9:
+        cases.append(("interpolate", th.pool_interp_faces(p, k, u, rng.integers(0, n_patch, n_face), nrm, sid,
+                                                          rng.integers(0, 9, n_face)), k * p * p))
+    for role, rec, ncell in cases:
+        op = th.operators.DEFAULT_CACHE.device_operator(role, scheme, p, k)
+        rec_t = _transpose_records(rec, E, u, patch)
+        outs = []
+        for s, r in ((src, rec), (src_t, rec_t)):
+            dst = torch.full((n_face * ncell * u,), np.nan, dtype=torch.float64, device=dev)
+            th.FaceBatch(op, r, u).launch(s, dst)
+            outs.append(dst.cpu().numpy())
+        assert np.isfinite(outs[0]).all()
+        assert np.array_equal(outs[0], outs[1]), (role, scheme, np.abs(outs[0] - outs[1]).max())
