@@ -1,23 +1,30 @@
-// order3 restriction with CTA-level staging (included by trihalo.cu after
-// gram_slide.cuh).
+// Slice-staged fixed-window kernels (included by trihalo.cu after gram_slide.cuh):
+// order3 restriction, and order2 / order3 / tensor_linear interpolation.
 //
-// What it computes is the reference's least-squares restriction
-// (taylor.py:171-219 rows, linear.py apply order) in the Gram-separable form of
-// gram_slide.cuh.  For a restriction face the t2 windows (L = 5 fine slices)
-// step by 3 and overlap by <= 2, so a fine slice feeds at most two coarse
-// columns, and the z-pass and t2 synthesis fold into one 1-D row per degree:
-//   Q_ab(j) = sum_z K_{a+b}(j, z) T_ab(w_j + z),  K_d(j, z) = sum_{c <= 3-d} S2_j[c] P_c(z)
-//   out_i   = sum_a S0_i[a] sum_b S1[b] Q_ab
-// with T_ab the per-slice x/y Gram moments.  Each consumer warp keeps the two
-// open windows' Q (20 doubles) in registers: no moment ring.
+// What they compute is gram_slide.cuh's: the reference's least-squares rows
+// (taylor.py:171-219) as the Gram-separable projection onto total degree <=
+// ORDER, or the d-linear 1-D rows contracted normal, t1, t2 (linear.py:115-151),
+// swept along t2 one source slice at a time.  What changes is who loads:
 //
-// Why staging: the per-warp slide is latency-bound (one 25-cell slice in
-// flight per warp, 12-16 warps/SM: 0.58 of HBM).  Here one CTA owns a
-// (face, t1 tile) and a producer warp streams the tile's fine slices -- planes
-// of NX (normal) x NY (t1) cells -- into an NST-stage shared-memory ring with
-// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx), so a whole plane
-// per stage is in flight without registers, and the t1-overlapping windows of
-// the tile's consumer warps read it from shared memory instead of L2.
+// The per-warp slide is latency-bound -- each warp has one window slice of
+// loads in flight and 12-16 warps fit per SM (0.28-0.59 of HBM).  Here one CTA
+// owns a (face, tile of t1 groups) and a PRODUCER warp streams the tile's
+// source slices -- planes of NX (normal) x NY (t1 range) cells -- into an
+// NST-stage shared-memory ring with 1-D TMA bulk copies (cp.async.bulk +
+// mbarrier complete_tx): whole planes in flight per SM without registers, and
+// the t1-overlapping windows of the tile's CONSUMER warps read them from
+// shared memory instead of L2.
+//
+// Consumers (one per t1 group x 32-unknown chunk of the tile):
+//   ROLE 1 (restriction, ORDER 3): t2 windows step by 3 and overlap by <= 2, so
+//     a slice feeds at most two coarse columns and the z-pass and t2 synthesis
+//     fold into one 1-D row per degree,
+//       Q_ab(j) = sum_z K_{a+b}(j, z) T_ab(w_j + z),  K_d(j, z) = sum_{c <= 3-d} S2_j[c] P_c(z),
+//       out_i   = sum_a S0_i[a] sum_b S1[b] Q_ab,
+//     the two open windows' Q living in registers (NU = 2 unknowns per lane).
+//   ROLE 0 (interpolation): t2 windows step by 1, so every slice's x/y moments go
+//     into a lane-private ring of L slices in shared memory (as gram_slide.cuh)
+//     and each completed block does its z-pass and synthesis from the ring.
 //
 // Bulk copies need 16-byte alignment; unpadded cells (u = 59: 472 B) are only
 // 8-byte aligned, and one copy per cell is op-rate bound (2.0 TB/s measured,
@@ -35,46 +42,52 @@
 
 namespace stage {
 
-constexpr int L = 5, D = 4, NT = 10;
-
 struct Tile {
-  int gA, gB, y0, ny;
+  int gA, gB, y0, ny, z0, z1;
 };
 
-__device__ __forceinline__ Tile tile_of(const DevOp& op, int ti, int ntiles) {
-  Tile t;
-  t.gA = ti * op.G1 / ntiles;
-  t.gB = (ti + 1) * op.G1 / ntiles;
+// tile ti of a face: t1 groups [gA, gB) of the face's range, their window union
+// [y0, y0 + ny) along t1 and the union [z0, z1) of all its t2 windows
+__device__ __forceinline__ bool tile_of(const DevOp& op, const FaceRef& fr, int ti, int tg, int L, Tile& t) {
+  t.gA = fr.g1 + ti * tg;
+  t.gB = min(fr.g1 + fr.n1, t.gA + tg);
+  if (fr.n0 != 1 || t.gA >= t.gB || fr.n2 < 1) return false;
   t.y0 = __ldg(&op.grp1[t.gA]).x;
   t.ny = __ldg(&op.grp1[t.gB - 1]).x + L - t.y0;
-  return t;
+  t.z0 = __ldg(&op.grp1[fr.g2]).x;
+  t.z1 = __ldg(&op.grp1[fr.g2 + fr.n2 - 1]).x + L;
+  return true;
 }
 
 __device__ __forceinline__ int round_even(int v) { return (v + 1) & ~1; }
 
 }  // namespace stage
 
-template <int NCW, int NST, int NU>
-__global__ void __launch_bounds__((NCW + 1) * 32, 1)
-    stage_restrict3_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
-                           const th_face* __restrict__ faces, int64_t n_faces, int u, int32_t* flag, int stage_d,
-                           int ny_max) {
+template <int ROLE, int ORDER, bool TENSOR, int NCW, int NST, int NU, int MINB>
+__global__ void __launch_bounds__((NCW + 1) * 32, MINB)
+    stage_slide_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
+                       const th_face* __restrict__ faces, int64_t n_faces, int u, int32_t* flag, int stage_d,
+                       int ny_max, int tg, int tiles_per_face) {
   using namespace stage;
+  constexpr int L = ORDER == 2 ? 3 : 5;
+  constexpr int D = ORDER + 1;
+  constexpr int NT = TENSOR ? 9 : (ORDER == 2 ? 6 : 10);  // per-slice values: pairs a + b <= ORDER
+  constexpr int NM = ORDER == 2 ? 10 : 20;                // triples a + b + c <= ORDER
+  static_assert(ROLE == 0 || (ORDER == 3 && !TENSOR), "restriction: order3 Gram only");
+  static_assert(ROLE == 1 || NU == 1, "interpolation: one unknown per lane");
   extern __shared__ __align__(128) double sm[];
-  double* const stages = sm;                                        // [NST][stage_d]
-  double* const ktab = sm + NST * stage_d;                          // [G1][L][D]
-  int* const hdr = reinterpret_cast<int*>(ktab + op.G1 * L * D);    // [NST][4]: XS, YS, BASE
-  unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);  // [NST][ny_max]
+  double* const stages = sm;                                                      // [NST][stage_d]
+  double* const ktab = sm + NST * stage_d;                                        // ROLE 1: [G1][L][D]
+  double* const rings = ktab + (ROLE == 1 ? op.G1 * L * D : 0);                   // ROLE 0: [NCW][L][NT][32]
+  int* const hdr = reinterpret_cast<int*>(rings + (ROLE == 0 ? NCW * L * NT * 32 : 0));  // [NST][4]
+  unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);             // [NST][ny_max]
   unsigned char* const shr = reinterpret_cast<unsigned char*>(eline + NST * ny_max);  // producer scratch
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int p = op.p, G1 = op.G1;
   const int nch = (u + 32 * NU - 1) / (32 * NU);
-  const int tg = min(G1, NCW / nch);
-  const int ntiles = (G1 + tg - 1) / tg;
-  const int64_t total = n_faces * ntiles;
-  const int a2lo = __ldg(&op.grp1[0]).x, a2hi = __ldg(&op.grp1[G1 - 1]).x + L;
+  const int64_t total = n_faces * tiles_per_face;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -83,13 +96,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
     mbar_fence_init();
   }
-  // K_d(j, z): the t2 synthesis folded into the z-pass (child 0 of each 1-child group)
-  for (int i = threadIdx.x; i < G1 * L * D; i += blockDim.x) {
-    const int g = i / (L * D), z = (i / D) % L, d = i % D;
-    const double* S = op.synth1 + g * 12;
-    double k = 0.0;
-    for (int c = 0; c + d < D; ++c) k = fma(__ldg(S + c), Gram<5>::P(c, z), k);
-    ktab[i] = k;
+  if constexpr (ROLE == 1) {
+    // K_d(j, z): the t2 synthesis folded into the z-pass (child 0 of each 1-child group)
+    for (int i = threadIdx.x; i < G1 * L * D; i += blockDim.x) {
+      const int g = i / (L * D), z = (i / D) % L, d = i % D;
+      const double* S = op.synth1 + g * 12;
+      double k = 0.0;
+      for (int c = 0; c + d < D; ++c) k = fma(__ldg(S + c), Gram<L>::P(c, z), k);
+      ktab[i] = k;
+    }
   }
   __syncthreads();
 
@@ -98,12 +113,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     int s = 0;
     unsigned ph = 0;
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int64_t f = tile / ntiles;
+      const int64_t f = tile / tiles_per_face;
       const th_face* fp = faces + f;
       FaceRef fr;
       decode_face(fp, op, fr);
-      if (fr.n0 != 1) continue;
-      const Tile t = tile_of(op, int(tile - f * ntiles), ntiles);
+      Tile t;
+      if (!tile_of(op, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
       const int4 G0 = __ldg(&op.grp0[fr.g0]);
       const int nx = G0.y, x0 = G0.x;
       const int64_t adj = fr.src0 - __ldg(&fp->src[0]);
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
       int64_t rbb[2] = {0, 0};
       int b2prev = -1;
-      for (int a2 = a2lo; a2 < a2hi; ++a2) {
+      for (int a2 = t.z0; a2 < t.z1; ++a2) {
         mbar_wait(&empty[s], ph ^ 1);
         const int b2 = a2 / p;
         const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
@@ -277,18 +292,19 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
   } else {
     // ===================== consumers =====================
+    if constexpr (ROLE == 1) {
     // warp w owns t1 group gA + w / nch and unknowns [cb, cb + 32 NU) of the tile;
     // lane q-th unknown = cb + lane + 32 q
     int s = 0;
     unsigned ph = 0;
     const int gi = warp / nch, chunk = warp - gi * nch;
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int64_t f = tile / ntiles;
+      const int64_t f = tile / tiles_per_face;
       const th_face* fp = faces + f;
       FaceRef fr;
       decode_face(fp, op, fr);
-      if (fr.n0 != 1) continue;
-      const Tile t = tile_of(op, int(tile - f * ntiles), ntiles);
+      Tile t;
+      if (!tile_of(op, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
       const bool active = gi < t.gB - t.gA && warp < tg * nch;
       const int g1 = t.gA + (active ? gi : 0);
       const int ly = __ldg(&op.grp1[g1]).x - t.y0;
@@ -305,7 +321,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       int wA = __ldg(&op.grp1[0]).x;
       int wB = G1 > 1 ? __ldg(&op.grp1[1]).x : INT_MAX / 2;
       bool bad = false;
-      for (int a2 = a2lo; a2 < a2hi; ++a2) {
+      for (int a2 = t.z0; a2 < t.z1; ++a2) {
         const int zA = a2 - wA, zB = a2 - wB;
         const bool inA = zA >= 0 && zA < L, inB = zB >= 0 && zB < L;
         mbar_wait(&full[s], ph);
@@ -412,6 +428,200 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
       }
       if (active) raise_flag(flag, bad);
+    }
+    } else {
+    // warp w owns t1 group gA + w / nch and unknowns [cb, cb + 32) of the tile
+    int s = 0;
+    unsigned ph = 0;
+    const int gi = warp / nch, chunk = warp - gi * nch;
+    double* const ring = rings + warp * (L * NT * 32) + lane;  // [slot][t] x 32 lanes, lane-private
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int64_t f = tile / tiles_per_face;
+      const th_face* fp = faces + f;
+      FaceRef fr;
+      decode_face(fp, op, fr);
+      Tile t;
+      if (!tile_of(op, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
+      const bool active = gi < t.gB - t.gA;
+      const int g1 = t.gA + (active ? gi : 0);
+      const int4 G0 = __ldg(&op.grp0[fr.g0]), Gy = __ldg(&op.grp1[g1]);
+      const int ly = Gy.x - t.y0;
+      const int cb = chunk * 32;
+      const bool ok = active && cb + lane < u;
+      double R0[TENSOR ? 3 : 1][TENSOR ? L : 1], R1[TENSOR ? 3 : 1][TENSOR ? L : 1];
+      if constexpr (TENSOR) {
+        const double* r0 = op.rows0 + __ldg(&op.row_off0[fr.g0]);
+        const double* r1 = op.rows1 + __ldg(&op.row_off1[g1]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int x = 0; x < L; ++x) {
+            R0[c][x] = c < G0.w ? __ldg(r0 + c * L + x) : 0.0;
+            R1[c][x] = c < Gy.w ? __ldg(r1 + c * L + x) : 0.0;
+          }
+      }
+      int gz = fr.g2;  // next t2 block to complete
+      const int gz_end = fr.g2 + fr.n2;
+      int wend = __ldg(&op.grp1[gz]).x + L - 1;
+      bool bad = false;
+      for (int a2 = t.z0; a2 < t.z1; ++a2) {
+        mbar_wait(&full[s], ph);
+        if (active) {
+          const int* h = hdr + s * 4;
+          const int XS = h[0], YS = h[1], BASE = h[2];
+          const double* st = stages + size_t(s) * stage_d + BASE + cb + lane;
+          const unsigned* el = eline + s * ny_max + ly;
+          double T[NT];
+#pragma unroll
+          for (int i = 0; i < NT; ++i) T[i] = 0.0;
+#pragma unroll
+          for (int y = 0; y < L; ++y) {
+            const unsigned e = el[y];
+            const double* ln = st + (ly + y) * YS;
+            double v[L];
+#pragma unroll
+            for (int x = 0; x < L; ++x) v[x] = ok ? ln[x * XS + int((e >> (6 * x)) & 63u)] : 0.0;
+            if constexpr (TENSOR) {
+#pragma unroll
+              for (int c0 = 0; c0 < 3; ++c0) {
+                double tx = 0.0;
+#pragma unroll
+                for (int x = 0; x < L; ++x) tx = fma(R0[c0][x], v[x], tx);
+#pragma unroll
+                for (int c1 = 0; c1 < 3; ++c1) T[c0 + 3 * c1] = fma(R1[c1][y], tx, T[c0 + 3 * c1]);
+              }
+            } else {
+              double m[D];
+#pragma unroll
+              for (int a = 0; a < D; ++a) {
+                m[a] = 0.0;
+#pragma unroll
+                for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[x]);
+              }
+              int tt = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) gacc(T[tt], Gram<L>::P(b, y), m[a]);
+            }
+          }
+          double* slot = ring + (a2 % L) * (NT * 32);
+#pragma unroll
+          for (int i = 0; i < NT; ++i) slot[i * 32] = T[i];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (!active) continue;
+        // ---- blocks whose window ends at this slice: z-pass + synthesis, store ----
+        while (gz < gz_end && wend <= a2) {
+          const int4 Gz = __ldg(&op.grp1[gz]);
+          const int slot0 = Gz.x % L;
+          double* const dbase = dst + fr.dst + cb + lane;
+          if constexpr (TENSOR) {
+            const double* r2 = op.rows1 + __ldg(&op.row_off1[gz]);
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+              const int tz = Gz.z + l;
+              if (!(l < Gz.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
+              const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
+              double o[NT];
+#pragma unroll
+              for (int i = 0; i < NT; ++i) o[i] = 0.0;
+#pragma unroll
+              for (int z = 0; z < L; ++z) {
+                const double w = ldg_slice(r2 + l * L + z);
+                const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
+                const double* slot = ring + sl * (NT * 32);
+#pragma unroll
+                for (int i = 0; i < NT; ++i) o[i] = fma(w, slot[i * 32], o[i]);
+              }
+#pragma unroll
+              for (int j = 0; j < 3; ++j) {
+                const int t1 = Gy.z + j;
+                if (!(j < Gy.w && t1 >= fr.lo1 && t1 < fr.lo1 + p)) continue;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                  const int t0 = G0.z + i;
+                  if (i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0 && ok) {
+                    dbase[int64_t(t0 - fr.lo0) * fr.dn + int64_t(t1 - fr.lo1) * fr.d1 + do2] = o[i + 3 * j];
+                    bad |= !isfinite(o[i + 3 * j]);
+                  }
+                }
+              }
+            }
+          } else {
+            double M[NM];
+#pragma unroll
+            for (int i = 0; i < NM; ++i) M[i] = 0.0;
+#pragma unroll
+            for (int z = 0; z < L; ++z) {
+              const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
+              const double* slot = ring + sl * (NT * 32);
+              int tt = 0, mi = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) {
+                  const double Tz = slot[tt * 32];
+#pragma unroll
+                  for (int c = 0; c + b + a < D; ++c, ++mi) gacc(M[mi], Gram<L>::P(c, z), Tz);
+                }
+            }
+            const double* s0 = op.synth0 + fr.g0 * 12;
+            const double* s1 = op.synth1 + g1 * 12;
+            const double* s2 = op.synth1 + gz * 12;
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+              const int tz = Gz.z + l;
+              if (!(l < Gz.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
+              const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
+              double Q[NT];
+              int tt = 0, mi = 0;
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b + a < D; ++b, ++tt) {
+                  Q[tt] = 0.0;
+#pragma unroll
+                  for (int c = 0; c + b + a < D; ++c, ++mi) Q[tt] = fma(__ldg(s2 + l * 4 + c), M[mi], Q[tt]);
+                }
+#pragma unroll
+              for (int j = 0; j < 3; ++j) {
+                const int t1 = Gy.z + j;
+                if (!(j < Gy.w && t1 >= fr.lo1 && t1 < fr.lo1 + p)) continue;
+                double R[D];
+                int t3 = 0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                  R[a] = 0.0;
+#pragma unroll
+                  for (int b = 0; b + a < D; ++b, ++t3) R[a] = fma(__ldg(s1 + j * 4 + b), Q[t3], R[a]);
+                }
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                  const int t0 = G0.z + i;
+                  if (!(i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0)) continue;
+                  double o = 0.0;
+#pragma unroll
+                  for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
+                  if (ok) {
+                    dbase[int64_t(t0 - fr.lo0) * fr.dn + int64_t(t1 - fr.lo1) * fr.d1 + do2] = o;
+                    bad |= !isfinite(o);
+                  }
+                }
+              }
+            }
+          }
+          ++gz;
+          if (gz < gz_end) wend = __ldg(&op.grp1[gz]).x + L - 1;
+        }
+      }
+      if (active) raise_flag(flag, bad);
+    }
     }
   }
 }

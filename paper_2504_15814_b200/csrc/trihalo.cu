@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "window.cuh"
 #include "restrict_pipe.cuh"
 #include "gram_slide.cuh"
-#include "stage_restrict.cuh"
+#include "stage_slide.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -450,30 +450,59 @@ void prepare_stage(th_operator* op) {
   op->st_ok = true;
 }
 
-// launch geometry of the staged restriction for u unknowns; false = does not fit
+// launch geometry of the slice-staged kernels (stage_slide.cuh) for u unknowns;
+// false = the operator / u does not fit them
 struct StageGeom {
-  int nst = 0, stage_d = 0, ny_max = 0;
+  int nst = 0, stage_d = 0, ny_max = 0, tg = 0, tiles_per_face = 0;
   size_t smem = 0;
 };
-constexpr int kStageNCW = 9, kStageNU = 2;  // consumer warps per CTA (one per t1 group at u <= 64), unknowns per lane
+constexpr int kRestrictNCW = 9, kRestrictNU = 2;  // restriction: one consumer warp per t1 group at u <= 64
+constexpr int kInterpNCW = 6;                      // interpolation: 3 t1 groups x 2 chunks of 32 at u <= 64
 
-bool stage_geometry(const th_operator* op, int u, StageGeom& g) {
+bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   const th::HostOperator& h = op->host;
-  const int G1 = (int)h.groups[1].size();
-  const int nch = (u + 32 * kStageNU - 1) / (32 * kStageNU);
-  if (nch > kStageNCW) return false;
-  const int tg = std::min(G1, kStageNCW / nch);
-  const int ntiles = (G1 + tg - 1) / tg;
-  g.ny_max = 0;
-  for (int t = 0; t < ntiles; ++t) {
-    const int gA = t * G1 / ntiles, gB = (t + 1) * G1 / ntiles;
-    g.ny_max = std::max(g.ny_max, h.groups[1][gB - 1].win0 + 5 - h.groups[1][gA].win0);
+  const bool interp = h.role == 0;
+  if (interp) {
+    if (h.groups[0].size() != 1 || h.fast_C0 != 3 || h.fast_CT != 3) return false;
+    const bool tensor = h.scheme == TH_SCHEME_TENSOR_LINEAR && h.fast_mode == 2 && h.fast_L0 == 3;
+    const bool gram = (h.scheme == TH_SCHEME_ORDER2 || h.scheme == TH_SCHEME_ORDER3) && h.gram_ok && h.fast_mode == 3;
+    if (!tensor && !gram) return false;
+  } else if (!op->st_ok) {
+    return false;
   }
-  g.stage_d = (5 * g.ny_max * (u + 3) + 1) & ~1;
-  const size_t tail = size_t(G1) * 20 * 8 + 16 * 4 /*hdr*/ + size_t(4) * g.ny_max * 4 + size_t(5) * g.ny_max + 64;
+  const int L = h.fast_L0 > 0 ? h.fast_L0 : 5;
+  const int ncw = interp ? kInterpNCW : kRestrictNCW, nu = interp ? 1 : kRestrictNU;
+  const int nch = (u + 32 * nu - 1) / (32 * nu);
+  if (nch > ncw) return false;
+  const auto& g1 = h.groups[1];
+  // t1 group ranges a tile may come from: the three segment columns (interpolation) or the face
+  std::vector<std::pair<int, int>> ranges;
+  if (interp) {
+    for (int sgi = 0; sgi < 3; ++sgi)
+      if (h.seg_g[sgi][1] > h.seg_g[sgi][0]) ranges.push_back({h.seg_g[sgi][0], h.seg_g[sgi][1]});
+  } else {
+    ranges.push_back({0, (int)g1.size()});
+  }
+  int max_n = 0;
+  for (auto& r : ranges) max_n = std::max(max_n, r.second - r.first);
+  if (max_n == 0) return false;
+  const int tiles = (max_n + ncw / nch - 1) / (ncw / nch);
+  g.tg = (max_n + tiles - 1) / tiles;
+  g.tiles_per_face = tiles;
+  g.ny_max = 0;
+  for (auto& r : ranges)
+    for (int ga = r.first; ga < r.second; ga += g.tg) {
+      const int gb = std::min(r.second, ga + g.tg);
+      g.ny_max = std::max(g.ny_max, g1[gb - 1].win0 + L - g1[ga].win0);
+    }
+  g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
+  const int NT = h.scheme == TH_SCHEME_TENSOR_LINEAR ? 9 : (L == 3 ? 6 : 10);
+  const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : size_t(g1.size()) * L * 4 * 8;
+  const size_t budget = size_t(227 * 1024) / size_t(minb) - 1024;
   for (int nst = 3; nst >= 2; --nst) {
-    const size_t smem = size_t(nst) * g.stage_d * 8 + tail;
-    if (smem <= 227 * 1024 - 1024) {
+    const size_t smem = size_t(nst) * g.stage_d * 8 + extra + size_t(nst) * 16 + size_t(nst) * g.ny_max * 4 +
+                        size_t(L) * g.ny_max + 64;
+    if (smem <= budget) {
       g.nst = nst;
       g.smem = smem;
       return true;
@@ -694,12 +723,33 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   } while (0)
   // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
   // (bit 1: interpolation, bit 2: order3 restriction)
-  // (bit 4: order3 restriction through the staged TMA kernel, stage_restrict.cuh;
+  // (bit 4: order3 restriction through the slice-staged TMA kernel, stage_slide.cuh;
   //  bit 8: tensor_linear interpolation through the slice ring)
   static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 15; }();
-  StageGeom sg;
   const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
-  if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
+  // slice-staged interpolation (stage_slide.cuh), off by default: TH_STAGE_INTERP=1 enables.
+  // Interpolation is store-bound (80% of its bytes are 472-byte-cell stores, which stream at
+  // 4.0-5.4 TB/s on B200: profiles/r01_probe_store.txt), so staging its loads measured equal
+  // to the per-warp slide on config 2 and 0.28 vs 0.31 on config 3 (profiles/r01_ab_stage.txt)
+  static const int stage_interp = [] { const char* e = std::getenv("TH_STAGE_INTERP"); return e ? std::atoi(e) : 0; }();
+  StageGeom sg;
+#define TH_SLIDE(ROLE, ORDER, TENSOR, NCW, NU, MINB)                                                          \
+  do {                                                                                                        \
+    auto kfn = sg.nst == 3 ? stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 3, NU, MINB>                        \
+                           : stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 2, NU, MINB>;                       \
+    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sg.smem)));           \
+    const int64_t tiles = n_faces * sg.tiles_per_face;                                                       \
+    const int sblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * MINB));                             \
+    kfn<<<sblocks, (NCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,      \
+                                                 sg.ny_max, sg.tg, sg.tiles_per_face);                        \
+  } while (0)
+  const int sminb = !interp ? 1 : h.scheme == TH_SCHEME_ORDER3 ? 1 : 2;
+  if (stage_interp && interp && stage_geometry(op, u, sminb, sg)) {
+    if (h.scheme == TH_SCHEME_ORDER3) TH_SLIDE(0, 3, false, kInterpNCW, 1, 1);
+    else if (h.scheme == TH_SCHEME_TENSOR_LINEAR) TH_SLIDE(0, 2, true, kInterpNCW, 1, 2);
+    else TH_SLIDE(0, 2, false, kInterpNCW, 1, 2);
+  }
+  else if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
     // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
     auto kfn = imin == 5 ? gram_slide_kernel<2, 0, 5, true> : gram_slide_kernel<2, 0, 4, true>;
     const size_t smem = size_t(4) * 3 * 9 * 32 * 8;
@@ -712,21 +762,15 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   else if (gram && interp && h.scheme == 2 && minbset) TH_GRAM(2, 0, 4);
   else if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
   else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && op->st_ok && stage_geometry(op, u, sg)) {
-    // staged order3 restriction: persistent, one CTA per SM (stage_restrict.cuh)
-    auto kfn = sg.nst == 3 ? stage_restrict3_kernel<kStageNCW, 3, kStageNU> : stage_restrict3_kernel<kStageNCW, 2, kStageNU>;
-    TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sg.smem)));
-    const int G1 = op->dev.G1, nch = (u + 32 * kStageNU - 1) / (32 * kStageNU);
-    const int tg = std::min(G1, kStageNCW / nch);
-    const int64_t tiles = n_faces * ((G1 + tg - 1) / tg);
-    const int sblocks = int(std::min<int64_t>(tiles, int64_t(num_sms())));
-    kfn<<<sblocks, (kStageNCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,
-                                                       sg.ny_max);
+  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && stage_geometry(op, u, 1, sg)) {
+    // slice-staged order3 restriction: persistent, one CTA per SM (stage_slide.cuh)
+    TH_SLIDE(1, 3, false, kRestrictNCW, kRestrictNU, 1);
   }
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 3) TH_GRAM(3, 1, 3);
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 5) TH_GRAM(3, 1, 5);
   else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
 #undef TH_GRAM
+#undef TH_SLIDE
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(1, 3, 1, 2, 6, 12);
   else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(2, 3, 1, 2, 6, 12);
   else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && minbset) TH_RREG(1, 3, 1, 2, 4, 8);

@@ -319,3 +319,20 @@ def test_pool_transposed_layout(th, scheme, p):
             outs.append(dst.cpu().numpy())
         assert np.isfinite(outs[0]).all()
         assert np.array_equal(outs[0], outs[1]), (role, scheme, np.abs(outs[0] - outs[1]).max())
+
+
+@pytest.mark.parametrize("env", ({"TH_STAGE_INTERP": "1"}, {"TH_GRAM": "3"}))
+def test_alternative_kernel_paths(th, env):
+    """Kernel choices are read once per process from the environment; re-run the
+    parity tests in a child process with the alternative paths (slice-staged
+    interpolation; the per-warp order3 restriction slide)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    res = subprocess.run(
+        [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_parity.py"),
+         "-k", "exchange_all_faces_small or pool_interp_batch or pool_restrict_batch or transposed"],
+        env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
