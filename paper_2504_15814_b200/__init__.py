@@ -46,5 +46,6 @@ from .schemes import (
     scheme_feasible,
 )
 from .faces import FaceBatch, pool_interp_faces, pool_restrict_faces, slab_faces
+from .csrio import dump_operator, dumps_operator, extract_half, extract_segment, from_triplets, load_operator
 
 __version__ = "0.1.0"
