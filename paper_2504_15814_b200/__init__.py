@@ -47,5 +47,14 @@ from .schemes import (
 )
 from .faces import FaceBatch, pool_interp_faces, pool_restrict_faces, slab_faces
 from .csrio import dump_operator, dumps_operator, extract_half, extract_segment, from_triplets, load_operator
+from .harness import (
+    BenchReport,
+    ConvergenceReport,
+    run_bench,
+    run_consistency_suite,
+    run_convergence,
+    run_unit_oracle,
+    sample_field,
+)
 
 __version__ = "0.1.0"
