@@ -224,8 +224,11 @@ def run_ours(args, rank, world, local_rank):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(f"config{s.config}", {})
-        result["roofline"]["traffic"] = tr.get(f"{passes[dom]['role']}:{passes[dom]['scheme']}")
-        result["roofline"]["traffic_source"] = "profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum)"
+        ent = tr.get(f"{passes[dom]['role']}:{passes[dom]['scheme']}")
+        if isinstance(ent, dict):  # bytes of one measured launch over its face count, scaled to this launch
+            result["roofline"]["traffic"] = round(ent["bytes"] * s.n_faces / ent["faces"])
+            result["roofline"]["traffic_source"] = (f"profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, "
+                                                    f"measured on {ent['faces']} faces, scaled per face)")
     except (OSError, ValueError):
         pass
     step_bytes = sum(ps["bytes"] for ps in passes)
