@@ -152,7 +152,8 @@ def test_unit_oracle_small_grid_and_skips(gpu):
 def test_unit_oracle_detects_corrupted_operator(gpu):
     def corrupt(op):
         v = op.values.copy()
-        v[0] += 0.37
+        if v.size:  # the outer half at k = 1 has no rows
+            v[0] += 0.37
         return CsrOperator(op.n_rows, op.n_cols, op.row_offsets, op.col_indices, v, op.scheme_tag, op.built_for,
                            op.source_region, op.target_region, op.max_condition)
 
