@@ -23,6 +23,8 @@ from .errors import (
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libtrihalo_b200.so")
+# A/B builds of the same ABI (tools/ab_build.sh): TH_LIBPATH points at another copy of the library
+LIB_PATH = os.environ.get("TH_LIBPATH", LIB_PATH)
 
 TH_OK, TH_ERR_CONFIG, TH_ERR_INFEASIBLE, TH_ERR_CONTRACT, TH_ERR_SINGULAR, TH_ERR_CUDA = range(6)
 ROLES = {"interpolate": 0, "restrict": 1}

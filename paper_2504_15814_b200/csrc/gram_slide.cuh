@@ -131,12 +131,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             }
           } else {
             double m[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-              m[a] = 0.0;
-#pragma unroll
-              for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[y][x]);
-            }
+            gram_moments<L, D>(v[y], m);
             int t = 0;
 #pragma unroll
             for (int a = 0; a < D; ++a)

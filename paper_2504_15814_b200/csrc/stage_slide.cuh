@@ -61,13 +61,129 @@ __device__ __forceinline__ bool tile_of(const DevOp& op, const FaceRef& fr, int 
 
 __device__ __forceinline__ int round_even(int v) { return (v + 1) & ~1; }
 
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Output staging of one interpolation block row (ROLE 0): the region normal children x
+// the tile's t1 children x this block's t2 children, laid out in shared memory as the
+// contiguous RUNS it forms in the target (the unit-stride axis, merged with the next axes
+// while contiguous), each run slot shifted by the run's 8-byte alignment so that its
+// 16-byte-aligned interior leaves with one cp.async.bulk store.
+struct OutPlan {
+  // target cell (a0 + i0, a1 + i1, a2 + i2) of the region lands in run  i . rm  at position
+  // pos0 + i . pm  (cells), and run r starts (lowest cell) at element  rs0 + i_outer . st_outer
+  int a0, a1, a2;
+  int pm0, pm1, pm2, pos0;
+  int rm0, rm1, rm2;
+  int64_t rsm0, rsm1, rsm2, rs0;
+  int n_o0;            // extent of the first outer axis (run-index decode)
+  int64_t st_o0, st_o1;
+  int R, nruns, rslot;
+
+  __device__ bool make(const int lo[3], const int hi[3], const FaceRef& fr, int u, int out_d) {
+    const int lob[3] = {fr.lo0, fr.lo1, fr.lo2};
+    const int64_t st[3] = {fr.dn, fr.d1, fr.d2};
+    int n[3];
+    int64_t base = fr.dst;
+    int merged = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      n[d] = hi[d] - lo[d];
+      base += int64_t(lo[d] - lob[d]) * st[d];
+      if (n[d] == 1) merged |= 1 << d;
+    }
+    if (n[0] <= 0 || n[1] <= 0 || n[2] <= 0) return false;
+    a0 = lo[0], a1 = lo[1], a2 = lo[2];
+    int inner = -1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (inner < 0 && n[d] > 1 && (st[d] == u || st[d] == -u)) inner = d;
+    if (inner < 0) return false;
+    merged |= 1 << inner;
+    int64_t span = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (d == inner) span = int64_t(n[d]) * u;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (!(merged >> d & 1) && (st[d] == span || st[d] == -span)) {
+          merged |= 1 << d;
+          span *= n[d];
+        }
+    R = int(span / u);
+    int pm[3], rm[3];
+    int64_t rsm[3];
+    pos0 = 0;
+    rs0 = base;
+    nruns = 1;
+    n_o0 = 1;
+    st_o0 = st_o1 = 0;
+    int nouter = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      pm[d] = 0, rm[d] = 0, rsm[d] = 0;
+      if (merged >> d & 1) {
+        if (n[d] > 1) {
+          const int w = int((st[d] > 0 ? st[d] : -st[d]) / u);
+          pm[d] = st[d] > 0 ? w : -w;
+          if (st[d] < 0) {
+            pos0 += (n[d] - 1) * w;
+            rs0 += int64_t(n[d] - 1) * st[d];
+          }
+        }
+      } else {
+        rsm[d] = st[d];
+        rm[d] = nouter == 0 ? 1 : n_o0;
+        if (nouter == 0) {
+          n_o0 = n[d];
+          st_o0 = st[d];
+        } else {
+          st_o1 = st[d];
+        }
+        nruns *= n[d];
+        ++nouter;
+      }
+    }
+    pm0 = pm[0], pm1 = pm[1], pm2 = pm[2];
+    rm0 = rm[0], rm1 = rm[1], rm2 = rm[2];
+    rsm0 = rsm[0], rsm1 = rsm[1], rsm2 = rsm[2];
+    rslot = round_even(R * u + 2);
+    return R * u * 8 >= 1024 && nruns * rslot <= out_d;
+  }
+  // shared-memory index (doubles, unknown 0) of target cell (t0, t1, t2)
+  __device__ __forceinline__ int index(const double* dst, int t0, int t1, int t2, int u) const {
+    const int i0 = t0 - a0, i1 = t1 - a1, i2 = t2 - a2;
+    const int r = i0 * rm0 + i1 * rm1 + i2 * rm2;
+    const int64_t start = rs0 + i0 * rsm0 + i1 * rsm1 + i2 * rsm2;
+    const int sh = int((reinterpret_cast<uintptr_t>(dst + start) & 15) >> 3);
+    return r * rslot + sh + (pos0 + i0 * pm0 + i1 * pm1 + i2 * pm2) * u;
+  }
+  // issue the bulk store of run r (16-byte-aligned interior) and its <= 2 edge doubles
+  __device__ void store(double* dst, const double* out, int r, int u) const {
+    const int64_t s0 = rs0 + int64_t(r % n_o0) * st_o0 + int64_t(r / n_o0) * st_o1;
+    double* g = dst + s0;
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(g), gend = ga + uintptr_t(R) * u * 8;
+    const uintptr_t lo = (ga + 15) & ~uintptr_t(15), hi = gend & ~uintptr_t(15);
+    const double* sm = out + r * rslot + int((ga & 15) >> 3);
+    if (hi > lo)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(lo),
+                   "r"(smem_u32(sm + (lo - ga) / 8)), "r"(unsigned(hi - lo))
+                   : "memory");
+    if (lo > ga) g[0] = sm[0];
+    if (gend > hi) g[R * u - 1] = sm[R * u - 1];
+  }
+};
+
 }  // namespace stage
 
 template <int ROLE, int ORDER, bool TENSOR, int NCW, int NST, int NU, int MINB>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     stage_slide_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
                        const th_face* __restrict__ faces, int64_t n_faces, int u, int32_t* flag, int stage_d,
-                       int ny_max, int tg, int tiles_per_face) {
+                       int ny_max, int tg, int tiles_per_face, int out_d) {
   using namespace stage;
   constexpr int L = ORDER == 2 ? 3 : 5;
   constexpr int D = ORDER + 1;
@@ -79,7 +195,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   double* const stages = sm;                                                      // [NST][stage_d]
   double* const ktab = sm + NST * stage_d;                                        // ROLE 1: [G1][L][D]
   double* const rings = ktab + (ROLE == 1 ? op.G1 * L * D : 0);                   // ROLE 0: [NCW][L][NT][32]
-  int* const hdr = reinterpret_cast<int*>(rings + (ROLE == 0 ? NCW * L * NT * 32 : 0));  // [NST][4]
+  double* const outbuf = rings + (ROLE == 0 ? NCW * L * NT * 32 : 0);             // ROLE 0: [out_d] output runs
+  int* const hdr = reinterpret_cast<int*>(outbuf + (ROLE == 0 ? out_d : 0));      // [NST][4]
   unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);             // [NST][ny_max]
   unsigned char* const shr = reinterpret_cast<unsigned char*>(eline + NST * ny_max);  // producer scratch
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
@@ -342,21 +459,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
             for (int y = 0; y < L; ++y) {
               const unsigned e = el[y];
               const double* ln = st + (ly + y) * YS + 32 * q;
-              double v[L];
+              double v[L], m[D];
 #pragma unroll
               for (int x = 0; x < L; ++x) v[x] = ok[q] ? ln[x * XS + int((e >> (6 * x)) & 63u)] : 0.0;
-              double m[D];
-#pragma unroll
-              for (int a = 0; a < D; ++a) {
-                m[a] = 0.0;
-#pragma unroll
-                for (int x = 0; x < L; ++x) gacc(m[a], Gram<5>::P(a, x), v[x]);
-              }
+              gram_moments<L, D>(v, m);  // x pass (symmetric form); y pass streamed below
               int tt = 0;
 #pragma unroll
               for (int a = 0; a < D; ++a)
 #pragma unroll
-                for (int b = 0; b + a < D; ++b, ++tt) gacc(T[tt], Gram<5>::P(b, y), m[a]);
+                for (int b = 0; b + a < D; ++b, ++tt) gacc(T[tt], Gram<L>::P(b, y), m[a]);
             }
             // z accumulation into the (at most two) open windows
             if (inA) {
@@ -492,12 +603,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
               }
             } else {
               double m[D];
-#pragma unroll
-              for (int a = 0; a < D; ++a) {
-                m[a] = 0.0;
-#pragma unroll
-                for (int x = 0; x < L; ++x) gacc(m[a], Gram<L>::P(a, x), v[x]);
-              }
+              gram_moments<L, D>(v, m);
               int tt = 0;
 #pragma unroll
               for (int a = 0; a < D; ++a)
@@ -515,19 +621,40 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
           s = 0;
           ph ^= 1;
         }
-        if (!active) continue;
         // ---- blocks whose window ends at this slice: z-pass + synthesis, store ----
+        // (uniform over the consumer warps: all of them take part in the output staging)
         while (gz < gz_end && wend <= a2) {
           const int4 Gz = __ldg(&op.grp1[gz]);
           const int slot0 = Gz.x % L;
           double* const dbase = dst + fr.dst + cb + lane;
-          if constexpr (TENSOR) {
+          OutPlan pl;
+          bool staged = false;
+          if (out_d > 0) {
+            const int4 Gl = __ldg(&op.grp1[t.gB - 1]), Gf = __ldg(&op.grp1[t.gA]);
+            const int lo[3] = {max(G0.z, fr.lo0), max(Gf.z, fr.lo1), max(Gz.z, fr.lo2)};
+            const int hi[3] = {min(G0.z + G0.w, fr.hi0), min(Gl.z + Gl.w, fr.lo1 + p), min(Gz.z + Gz.w, fr.lo2 + p)};
+            staged = pl.make(lo, hi, fr, u, out_d);
+          }
+          if (staged) {
+            // the previous row's bulk stores have finished reading the buffer
+            if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            named_bar(1, NCW * 32);
+          }
+          auto emit = [&](int t0, int t1, int t2, double o) {
+            if (!ok) return;
+            bad |= !isfinite(o);
+            if (staged)
+              outbuf[pl.index(dst, t0, t1, t2, u) + cb + lane] = o;
+            else
+              dbase[int64_t(t0 - fr.lo0) * fr.dn + int64_t(t1 - fr.lo1) * fr.d1 + int64_t(t2 - fr.lo2) * fr.d2] = o;
+          };
+          if (!active) {
+          } else if constexpr (TENSOR) {
             const double* r2 = op.rows1 + __ldg(&op.row_off1[gz]);
 #pragma unroll
             for (int l = 0; l < 3; ++l) {
               const int tz = Gz.z + l;
               if (!(l < Gz.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
-              const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
               double o[NT];
 #pragma unroll
               for (int i = 0; i < NT; ++i) o[i] = 0.0;
@@ -546,10 +673,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                   const int t0 = G0.z + i;
-                  if (i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0 && ok) {
-                    dbase[int64_t(t0 - fr.lo0) * fr.dn + int64_t(t1 - fr.lo1) * fr.d1 + do2] = o[i + 3 * j];
-                    bad |= !isfinite(o[i + 3 * j]);
-                  }
+                  if (i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) emit(t0, t1, tz, o[i + 3 * j]);
                 }
               }
             }
@@ -578,7 +702,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
             for (int l = 0; l < 3; ++l) {
               const int tz = Gz.z + l;
               if (!(l < Gz.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
-              const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
               double Q[NT];
               int tt = 0, mi = 0;
 #pragma unroll
@@ -608,12 +731,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
                   double o = 0.0;
 #pragma unroll
                   for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
-                  if (ok) {
-                    dbase[int64_t(t0 - fr.lo0) * fr.dn + int64_t(t1 - fr.lo1) * fr.d1 + do2] = o;
-                    bad |= !isfinite(o);
-                  }
+                  emit(t0, t1, tz, o);
                 }
               }
+            }
+          }
+          if (staged) {
+            // generic-proxy writes -> visible to the bulk (async-proxy) reads, then one warp stores
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            named_bar(1, NCW * 32);
+            if (warp == 0) {
+              for (int r = lane; r < pl.nruns; r += 32) pl.store(dst, outbuf, r, u);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
           }
           ++gz;
@@ -622,6 +751,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       }
       if (active) raise_flag(flag, bad);
     }
+    if (warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
 }

@@ -453,7 +453,7 @@ void prepare_stage(th_operator* op) {
 // launch geometry of the slice-staged kernels (stage_slide.cuh) for u unknowns;
 // false = the operator / u does not fit them
 struct StageGeom {
-  int nst = 0, stage_d = 0, ny_max = 0, tg = 0, tiles_per_face = 0;
+  int nst = 0, stage_d = 0, ny_max = 0, tg = 0, tiles_per_face = 0, out_d = 0;
   size_t smem = 0;
 };
 constexpr int kRestrictNCW = 9, kRestrictNU = 2;  // restriction: one consumer warp per t1 group at u <= 64
@@ -498,16 +498,22 @@ bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
   const int NT = h.scheme == TH_SCHEME_TENSOR_LINEAR ? 9 : (L == 3 ? 6 : 10);
   const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : size_t(g1.size()) * L * 4 * 8;
+  // interpolation output staging (TMA bulk stores of contiguous target runs): one block row of
+  // <= 3 normal x 3 tg t1 x 3 t2 children; TH_STAGE_OUT=0 disables (direct stores)
+  static const int stage_out = [] { const char* e = std::getenv("TH_STAGE_OUT"); return e ? std::atoi(e) : 1; }();
+  const int out_want = interp && stage_out ? ((3 * 3 * g.tg * 3 * (u + 3) + 1) & ~1) : 0;
   const size_t budget = size_t(227 * 1024) / size_t(minb) - 1024;
-  for (int nst = 3; nst >= 2; --nst) {
-    const size_t smem = size_t(nst) * g.stage_d * 8 + extra + size_t(nst) * 16 + size_t(nst) * g.ny_max * 4 +
-                        size_t(L) * g.ny_max + 64;
-    if (smem <= budget) {
-      g.nst = nst;
-      g.smem = smem;
-      return true;
+  for (int out_d : {out_want, 0})
+    for (int nst = 3; nst >= 2; --nst) {
+      const size_t smem = size_t(nst) * g.stage_d * 8 + extra + size_t(out_d) * 8 + size_t(nst) * 16 +
+                          size_t(nst) * g.ny_max * 4 + size_t(L) * g.ny_max + 64;
+      if (smem <= budget) {
+        g.nst = nst;
+        g.smem = smem;
+        g.out_d = out_d;
+        return true;
+      }
     }
-  }
   return false;
 }
 
@@ -741,7 +747,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int64_t tiles = n_faces * sg.tiles_per_face;                                                       \
     const int sblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * MINB));                             \
     kfn<<<sblocks, (NCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,      \
-                                                 sg.ny_max, sg.tg, sg.tiles_per_face);                        \
+                                                 sg.ny_max, sg.tg, sg.tiles_per_face, sg.out_d);              \
   } while (0)
   const int sminb = !interp ? 1 : h.scheme == TH_SCHEME_ORDER3 ? 1 : 2;
   if (stage_interp && interp && stage_geometry(op, u, sminb, sg)) {

@@ -38,6 +38,47 @@ struct Gram<5> {  // points {-2..2}: 1 | x | x^2 - 2 | (5x^3 - 17x) / 6
   }
 };
 
+// The first N discrete Gram moments  m_a = sum_x P_a(x) v[x]  of an L-point window,
+// through the weights' symmetry about the centre (pair sums / differences):
+//   L = 5:  m0 = s04 + s13 + v2, m1 = 2 d40 + d31, m2 = 2 (s04 - v2) - s13, m3 = d40 - 2 d31
+//   L = 3:  m0 = s02 + v1,       m1 = v2 - v0,     m2 = s02 - 2 v1
+// (10 / 4 FP64 ops instead of 18 / 6; rounding differs from the sequential sum by ~1 ulp)
+template <int L, int N>
+__device__ __forceinline__ void gram_moments(const double (&v)[L], double (&m)[N]) {
+  static_assert(L == 3 || L == 5, "Gram windows of 3 or 5 points");
+  if constexpr (L == 5) {
+    const double s04 = v[0] + v[4], s13 = v[1] + v[3];
+    m[0] = (s04 + s13) + v[2];
+    if constexpr (N > 1) {
+      const double d40 = v[4] - v[0], d31 = v[3] - v[1];
+      m[1] = fma(2.0, d40, d31);
+      if constexpr (N > 2) m[2] = fma(2.0, s04 - v[2], -s13);
+      if constexpr (N > 3) m[3] = fma(-2.0, d31, d40);
+    }
+  } else {
+    const double s02 = v[0] + v[2];
+    m[0] = s02 + v[1];
+    if constexpr (N > 1) m[1] = v[2] - v[0];
+    if constexpr (N > 2) m[2] = fma(-2.0, v[1], s02);
+  }
+}
+
+// y-pass of the per-line x moments mm[y][a]: T_ab = sum_y P_b(y) mm[y][a] for a + b < D,
+// pairs ordered a-major (T index = a D - a(a-1)/2 + b), each column through gram_moments
+template <int L, int D, int A = 0, int NT>
+__device__ __forceinline__ void gram_y(const double (&mm)[L][D], double (&T)[NT]) {
+  if constexpr (A < D) {
+    constexpr int OFF = A * D - A * (A - 1) / 2;
+    double col[L], tb[D - A];
+#pragma unroll
+    for (int y = 0; y < L; ++y) col[y] = mm[y][A];
+    gram_moments<L, D - A>(col, tb);
+#pragma unroll
+    for (int b = 0; b < D - A; ++b) T[OFF + b] = tb[b];
+    gram_y<L, D, A + 1>(mm, T);
+  }
+}
+
 // acc += g * v for a compile-time integer weight g (adds / subs when |g| = 1)
 __device__ __forceinline__ void gacc(double& acc, double g, double v) {
   if (g == 1.0) acc += v;
@@ -216,13 +257,10 @@ __global__ void __launch_bounds__(128, MINB) window_kernel(DevOp op, const doubl
             } else {
 #pragma unroll
               for (int q = 0; q < NU; ++q) {
-                double m[D];
+                double m[D], vx[L0];
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                  m[a] = 0.0;
-#pragma unroll
-                  for (int x = 0; x < L0; ++x) gacc(m[a], Gram<L0>::P(a, x), v[y][x][q]);
-                }
+                for (int x = 0; x < L0; ++x) vx[x] = v[y][x][q];
+                gram_moments<L0, D>(vx, m);
                 int t = 0;
 #pragma unroll
                 for (int a = 0; a < D; ++a)
