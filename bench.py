@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--reverse-passes", action="store_true", help="run the step's passes in reverse order (diagnosis)")
     return ap.parse_args()
 
 
@@ -136,7 +137,7 @@ def run_ours(args, rank, world, local_rank):
     p, k, u = s.p, s.k, s.u
     passes = []
     cache = th.operators.DEFAULT_CACHE
-    for role, scheme in s.passes:
+    for role, scheme in (reversed(s.passes) if args.reverse_passes else s.passes):
         op = cache.device_operator(role, scheme, p, k)
         if role == "interpolate":
             rec, src, ids = W.interp_records(wl), wl.pool, wl.interp_ids
