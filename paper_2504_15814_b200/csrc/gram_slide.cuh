@@ -94,6 +94,20 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
 #pragma unroll
         for (int y = 0; y < L; ++y) R1[c][y] = c < G1.w ? __ldg(r1 + c * L + y) : 0.0;
     }
+    if (ROLE == 0 && (op.prefetch & 8)) {
+      // L2 prefetch of the unit's whole source window (this chunk's <= 3 lines of every cell)
+      // through the LSU, so that the slices walked below load at L2 rather than DRAM latency
+      // (config 2 interpolation 0.55 -> 0.61 / 0.47 -> 0.51 of HBM; prefetching the warp's
+      //  next unit as well measured slower: profiles/r01_ab_stage.txt)
+      const int z0 = __ldg(&op.grp1[fr.g2]).x, nz = __ldg(&op.grp1[fr.g2 + fr.n2 - 1]).x + L - z0;
+      const char* const c0 = reinterpret_cast<const char*>(src + (ibase - lane + int64_t(z0) * fr.s2));
+      for (int i = lane; i < L * L * nz * 3; i += 32) {
+        const int cell = i / 3, part = i - cell * 3;
+        const int x = cell % L, y = (cell / L) % L, z = cell / (L * L);
+        l2_prefetch_line(c0 + 8 * (int64_t(x) * fr.sn + int64_t(y) * fr.s1 + int64_t(z) * fr.s2) +
+                         (part == 2 ? 255 : part * 128));
+      }
+    }
     int hi = -1;  // highest t2 source slice held in the ring
     for (int g2 = fr.g2; g2 < fr.g2 + fr.n2; ++g2) {
       const int4 G2 = __ldg(&op.grp1[g2]);

@@ -601,7 +601,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   d.n_blocks = (int32_t)h.block_off.size();
   {
     const char* e = std::getenv("TH_PREFETCH");
-    d.prefetch = e ? std::atoi(e) : 1;
+    d.prefetch = e ? std::atoi(e) : 9;  // bit 1: restriction window bulk prefetch, bit 8: interp unit windows
   }
   d.units_per_face = 0;
   d.ns_t = h.ax[1].ns;
