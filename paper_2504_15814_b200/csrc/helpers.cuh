@@ -27,7 +27,7 @@ __device__ __forceinline__ void l2_prefetch_line(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// ---- mbarrier + 1-D TMA bulk copy (stage_restrict.cuh) ----------------------
+// ---- mbarrier + 1-D TMA bulk copy (stage_slide.cuh) --------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");

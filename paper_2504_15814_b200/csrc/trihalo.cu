@@ -374,7 +374,7 @@ struct th_operator {
   // restriction register kernel: mode (0 = not eligible), window, classes, params blob
   int r_mode = 0, r_L = 0, r_ncls = 0;
   std::vector<unsigned char> r_params;
-  // staged order3 restriction (stage_restrict.cuh) eligibility
+  // staged order3 restriction (stage_slide.cuh) eligibility
   bool st_ok = false;
 };
 
@@ -428,7 +428,7 @@ void prepare_restrict(th_operator* op) {
   }
 }
 
-// eligibility of the staged order3 restriction (stage_restrict.cuh): every face
+// eligibility of the staged order3 restriction (stage_slide.cuh): every face
 // half has one normal group (5-cell window, <= 3 children); tangential groups
 // have 5-cell windows and one child, starts non-decreasing, and window j + 2
 // starts after window j ends (a fine slice feeds at most two coarse columns)
@@ -710,14 +710,6 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int rblocks = int(std::min<int64_t>((warps_needed + 3) / 4, int64_t(num_sms()) * CTAS));    \
     restrict_reg_kernel<MODE, L, NCLS, NU, MINB><<<rblocks, 128, 0, s>>>(op->dev, *prm, src, dst, faces, n_faces, u, flag); \
   } while (0)
-  // TH_RESTRICT_NU=1 selects the one-unknown-per-lane variant (tuning experiments)
-  static const int rnu = [] { const char* e = std::getenv("TH_RESTRICT_NU"); return e && e[0] == '1' ? 1 : 2; }();
-  static const int rminb = [] { const char* e = std::getenv("TH_RMINB"); return e ? std::atoi(e) : 5; }();
-  static const int gminb = [] { const char* e = std::getenv("TH_GMINB"); return e ? std::atoi(e) : 3; }();
-  // register budgets chosen so that no hot kernel spills (spills measured 25-35% slower);
-  // TH_MINBSET=0 restores the earlier, tighter budgets for A/B runs
-  static const int minbset = [] { const char* e = std::getenv("TH_MINBSET"); return e ? std::atoi(e) : 1; }();
-  static const int imin = [] { const char* e = std::getenv("TH_IMINB"); return e ? std::atoi(e) : 0; }();  // A/B
 #define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
   do {                                                                                                 \
     auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
@@ -727,18 +719,6 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * MINB * 2));       \
     kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);                        \
   } while (0)
-  // TH_GRAM=0 disables the Gram sliding kernels (A/B experiments)
-  // (bit 1: interpolation, bit 2: order3 restriction)
-  // (bit 4: order3 restriction through the slice-staged TMA kernel, stage_slide.cuh;
-  //  bit 8: tensor_linear interpolation through the slice ring)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 15; }();
-  const bool gram = use_gram && h.gram_ok && h.fast_C0 == 3;
-  // slice-staged interpolation (stage_slide.cuh), off by default: TH_STAGE_INTERP=1 enables.
-  // Interpolation is store-bound (80% of its bytes are 472-byte-cell stores, which stream at
-  // 4.0-5.4 TB/s on B200: profiles/r01_probe_store.txt), so staging its loads measured equal
-  // to the per-warp slide on config 2 and 0.28 vs 0.31 on config 3 (profiles/r01_ab_stage.txt)
-  static const int stage_interp = [] { const char* e = std::getenv("TH_STAGE_INTERP"); return e ? std::atoi(e) : 0; }();
-  StageGeom sg;
 #define TH_SLIDE(ROLE, ORDER, TENSOR, NCW, NU, MINB)                                                          \
   do {                                                                                                        \
     auto kfn = sg.nst == 3 ? stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 3, NU, MINB>                        \
@@ -749,44 +729,43 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     kfn<<<sblocks, (NCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,      \
                                                  sg.ny_max, sg.tg, sg.tiles_per_face, sg.out_d);              \
   } while (0)
-  const int sminb = !interp ? 1 : h.scheme == TH_SCHEME_ORDER3 ? 1 : 2;
-  if (stage_interp && interp && stage_geometry(op, u, sminb, sg)) {
+  // Kernel choice: the measured defaults (profiles/r01_ab_*.txt); register budgets are the
+  // largest occupancies at which the hot kernels do not spill.  Environment switches, read
+  // once per process, exist for A/B runs and are exercised by the GPU tests:
+  //   TH_GRAM bits (default 15)  1: Gram slide for order2 / order3 interpolation
+  //                              2: Gram slide for order3 restriction (fallback of bit 4)
+  //                              4: slice-staged order3 restriction (stage_slide.cuh)
+  //                              8: tensor_linear interpolation through the slice ring
+  //   TH_STAGE_INTERP=1          slice-staged interpolation (off: no faster than the slide,
+  //                              interpolation is bound by its per-warp latency and its 472-byte
+  //                              cell stores, profiles/r01_ab_stage.txt, r01_probe_store.txt)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 15; }();
+  static const int stage_interp = [] { const char* e = std::getenv("TH_STAGE_INTERP"); return e ? std::atoi(e) : 0; }();
+  const bool gram = h.gram_ok && h.fast_C0 == 3;
+  const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
+  StageGeom sg;
+  if (stage_interp && interp && stage_geometry(op, u, h.scheme == TH_SCHEME_ORDER3 ? 1 : 2, sg)) {
     if (h.scheme == TH_SCHEME_ORDER3) TH_SLIDE(0, 3, false, kInterpNCW, 1, 1);
     else if (h.scheme == TH_SCHEME_TENSOR_LINEAR) TH_SLIDE(0, 2, true, kInterpNCW, 1, 2);
     else TH_SLIDE(0, 2, false, kInterpNCW, 1, 2);
-  }
-  else if ((use_gram & 8) && interp && h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) {
+  } else if ((use_gram & 8) && interp && tensor_fast) {
     // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
-    auto kfn = imin == 5 ? gram_slide_kernel<2, 0, 5, true> : gram_slide_kernel<2, 0, 4, true>;
+    auto kfn = gram_slide_kernel<2, 0, 4, true>;
     const size_t smem = size_t(4) * 3 * 9 * 32 * 8;
     const int64_t units = n_faces * int64_t(op->dev.units_per_face) * ((u + 31) / 32);
     const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * 8));
     kfn<<<gblocks, 128, smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag);
   }
-  else if (gram && interp && h.scheme == 2 && imin == 3) TH_GRAM(2, 0, 3);
-  else if (gram && interp && h.scheme == 3 && imin == 2) TH_GRAM(3, 0, 2);
-  else if (gram && interp && h.scheme == 2 && minbset) TH_GRAM(2, 0, 4);
-  else if (gram && interp && h.scheme == 2) TH_GRAM(2, 0, 5);
-  else if (gram && interp && h.scheme == 3) TH_GRAM(3, 0, 3);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 4) && stage_geometry(op, u, 1, sg)) {
-    // slice-staged order3 restriction: persistent, one CTA per SM (stage_slide.cuh)
-    TH_SLIDE(1, 3, false, kRestrictNCW, kRestrictNU, 1);
-  }
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 3) TH_GRAM(3, 1, 3);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 2) && gminb == 5) TH_GRAM(3, 1, 5);
-  else if (gram && !interp && h.scheme == 3 && (use_gram & 2)) TH_GRAM(3, 1, 4);
+  else if (gram && (use_gram & 1) && interp && h.scheme == TH_SCHEME_ORDER2) TH_GRAM(2, 0, 4);
+  else if (gram && (use_gram & 1) && interp && h.scheme == TH_SCHEME_ORDER3) TH_GRAM(3, 0, 3);
+  else if (gram && (use_gram & 4) && !interp && h.scheme == TH_SCHEME_ORDER3 && stage_geometry(op, u, 1, sg))
+    TH_SLIDE(1, 3, false, kRestrictNCW, kRestrictNU, 1);  // persistent, one CTA per SM
+  else if (gram && (use_gram & 2) && !interp && h.scheme == TH_SCHEME_ORDER3) TH_GRAM(3, 1, 3);
 #undef TH_GRAM
 #undef TH_SLIDE
-  else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(1, 3, 1, 2, 6, 12);
-  else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2 && rminb == 6) TH_RREG(2, 3, 1, 2, 6, 12);
-  else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2 && minbset) TH_RREG(1, 3, 1, 2, 4, 8);
-  else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2 && minbset) TH_RREG(2, 3, 1, 2, 4, 8);
-  else if (op->r_mode == 1 && op->r_L == 3 && rnu == 2) TH_RREG(1, 3, 1, 2, 5, 10);
-  else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 1, 6, 12);
-  else if (op->r_mode == 1 && op->r_L == 5 && rnu == 2) TH_RREG(1, 5, 9, 2, 4, 8);
-  else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 1, 5, 10);
-  else if (op->r_mode == 2 && op->r_L == 3 && rnu == 2) TH_RREG(2, 3, 1, 2, 5, 10);
-  else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 1, 6, 12);
+  else if (op->r_mode == 1 && op->r_L == 3) TH_RREG(1, 3, 1, 2, 4, 8);
+  else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 2, 4, 8);
+  else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 2, 4, 8);
 #undef TH_RREG
   else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0, 3);
   else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0, 3);
