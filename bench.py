@@ -58,6 +58,10 @@ def peaks():
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms; only samples taken inside the
+    timed region (mark() .. stop()) are reported (the nearest one before it if the region is
+    shorter than the sampling interval)."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
 
@@ -65,6 +69,16 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.path = None
+        self.t_mark = None
+
+    def _rows(self):
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 6 and parts[0].isdigit():
+                    rows.append(parts)
+        return rows
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -75,25 +89,31 @@ class ClockSampler:
                  "-lms", "20", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        deadline = time.time() + 5.0  # nvidia-smi needs a moment before its first sample
+        while time.time() < deadline and not self._rows():
+            time.sleep(0.02)
+
+    def mark(self):
+        """Start of the timed region."""
+        self.n_before = len(self._rows()) if self.proc is not None else 0
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.03)  # let the sample covering the end of the region land
         self.proc.terminate()
         self.proc.wait()
-        rows = []
-        with open(self.path) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) == 6 and parts[0].isdigit():
-                    rows.append(parts)
+        rows = self._rows()
         os.unlink(self.path)
-        if not rows:
+        start = getattr(self, "n_before", 0)
+        inside = rows[start:] if len(rows) > start else rows[-1:]
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({names[i] for r in inside for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in inside), "sm_max_mhz": float(inside[0][1]),
+                "reasons": reasons, "samples": len(inside)}
 
 
 # ---------------------------------------------------------------------------
@@ -177,6 +197,7 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark()
     t0.record(stream)
     for kk in range(args.steps):
         step(ev_all[kk])
@@ -284,6 +305,7 @@ def run_multi(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    sampler.mark()
     t0.record(stream)
     for _ in range(args.steps):
         sweep.run(comp)

@@ -193,8 +193,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   static_assert(ROLE == 1 || NU == 1, "interpolation: one unknown per lane");
   extern __shared__ __align__(128) double sm[];
   double* const stages = sm;                                                      // [NST][stage_d]
-  double* const ktab = sm + NST * stage_d;                                        // ROLE 1: [G1][L][D]
-  double* const rings = ktab + (ROLE == 1 ? op.G1 * L * D : 0);                   // ROLE 0: [NCW][L][NT][32]
+  double* const wtab = sm + NST * stage_d;                  // ROLE 1: [class pair][z][y][a] folded weights
+  double* const rings = wtab + (ROLE == 1 ? op.st_ncls * op.st_ncls * 100 : 0);   // ROLE 0: [NCW][L][NT][32]
   double* const outbuf = rings + (ROLE == 0 ? NCW * L * NT * 32 : 0);             // ROLE 0: [out_d] output runs
   int* const hdr = reinterpret_cast<int*>(outbuf + (ROLE == 0 ? out_d : 0));      // [NST][4]
   unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);             // [NST][ny_max]
@@ -214,14 +214,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     mbar_fence_init();
   }
   if constexpr (ROLE == 1) {
-    // K_d(j, z): the t2 synthesis folded into the z-pass (child 0 of each 1-child group)
-    for (int i = threadIdx.x; i < G1 * L * D; i += blockDim.x) {
-      const int g = i / (L * D), z = (i / D) % L, d = i % D;
-      const double* S = op.synth1 + g * 12;
-      double k = 0.0;
-      for (int c = 0; c + d < D; ++c) k = fma(__ldg(S + c), Gram<L>::P(c, z), k);
-      ktab[i] = k;
-    }
+    // W_a(y, z) of every (t1, t2) synthesis-row class pair (host-built, trihalo.cu prepare_stage)
+    for (int i = threadIdx.x; i < op.st_ncls * op.st_ncls * 100; i += blockDim.x) wtab[i] = __ldg(op.st_w + i);
   }
   __syncthreads();
 
@@ -411,10 +405,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     // ===================== consumers =====================
     if constexpr (ROLE == 1) {
     // warp w owns t1 group gA + w / nch and unknowns [cb, cb + 32 NU) of the tile;
-    // lane q-th unknown = cb + lane + 32 q
+    // lane q-th unknown = cb + lane + 32 q.  Per slice and t1 line: the normal Gram moments
+    // m_a (gram_moments), then U_a += W_a(y, z) m_a for the <= 2 open t2 windows (A = j,
+    // B = j + 1); a window is complete after its 5th slice: out_i = sum_a S0_i[a] U_a.
     int s = 0;
     unsigned ph = 0;
     const int gi = warp / nch, chunk = warp - gi * nch;
+    const int ncl = op.st_ncls;
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int64_t f = tile / tiles_per_face;
       const th_face* fp = faces + f;
@@ -425,18 +422,20 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       const bool active = gi < t.gB - t.gA && warp < tg * nch;
       const int g1 = t.gA + (active ? gi : 0);
       const int ly = __ldg(&op.grp1[g1]).x - t.y0;
+      const double* const wrow = wtab + __ldg(&op.st_cls[g1]) * ncl * 100;  // + c2 * 100 per window
       const int cb = chunk * 32 * NU;
       bool ok[NU];
 #pragma unroll
       for (int q = 0; q < NU; ++q) ok[q] = active && cb + lane + 32 * q < u;
-      double QA[NU][NT], QB[NU][NT];
+      double UA[NU][D], UB[NU][D];
 #pragma unroll
       for (int q = 0; q < NU; ++q)
 #pragma unroll
-        for (int i = 0; i < NT; ++i) QA[q][i] = QB[q][i] = 0.0;
+        for (int i = 0; i < D; ++i) UA[q][i] = UB[q][i] = 0.0;
       int j = 0;
       int wA = __ldg(&op.grp1[0]).x;
       int wB = G1 > 1 ? __ldg(&op.grp1[1]).x : INT_MAX / 2;
+      int cA = __ldg(&op.st_cls[0]), cB = G1 > 1 ? __ldg(&op.st_cls[1]) : 0;
       bool bad = false;
       for (int a2 = t.z0; a2 < t.z1; ++a2) {
         const int zA = a2 - wA, zB = a2 - wB;
@@ -447,42 +446,29 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
           const int XS = h[0], YS = h[1], BASE = h[2];
           const double* st = stages + size_t(s) * stage_d + BASE + cb + lane;
           const unsigned* el = eline + s * ny_max + ly;
-          const double* kA = ktab + (j * L + (inA ? zA : 0)) * D;
-          const double* kB = ktab + ((j + 1) * L + (inB ? zB : 0)) * D;
-          // one unknown at a time: only one T[] live next to the open windows' Q
+          const double* wa = wrow + cA * 100 + (inA ? zA : 0) * 20;
+          const double* wb = wrow + cB * 100 + (inB ? zB : 0) * 20;
 #pragma unroll
-          for (int q = 0; q < NU; ++q) {
-            double T[NT];
+          for (int y = 0; y < L; ++y) {
+            const unsigned e = el[y];
+            const double* ln = st + (ly + y) * YS;
+            double WA[D], WB[D];
 #pragma unroll
-            for (int i = 0; i < NT; ++i) T[i] = 0.0;
+            for (int i = 0; i < D; ++i) {
+              WA[i] = inA ? wa[y * 4 + i] : 0.0;
+              WB[i] = inB ? wb[y * 4 + i] : 0.0;
+            }
 #pragma unroll
-            for (int y = 0; y < L; ++y) {
-              const unsigned e = el[y];
-              const double* ln = st + (ly + y) * YS + 32 * q;
+            for (int q = 0; q < NU; ++q) {
               double v[L], m[D];
 #pragma unroll
-              for (int x = 0; x < L; ++x) v[x] = ok[q] ? ln[x * XS + int((e >> (6 * x)) & 63u)] : 0.0;
-              gram_moments<L, D>(v, m);  // x pass (symmetric form); y pass streamed below
-              int tt = 0;
+              for (int x = 0; x < L; ++x) v[x] = ok[q] ? ln[x * XS + int((e >> (6 * x)) & 63u) + 32 * q] : 0.0;
+              gram_moments<L, D>(v, m);
 #pragma unroll
-              for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int b = 0; b + a < D; ++b, ++tt) gacc(T[tt], Gram<L>::P(b, y), m[a]);
-            }
-            // z accumulation into the (at most two) open windows
-            if (inA) {
-              int tt = 0;
-#pragma unroll
-              for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int b = 0; b + a < D; ++b, ++tt) QA[q][tt] = fma(kA[a + b], T[tt], QA[q][tt]);
-            }
-            if (inB) {
-              int tt = 0;
-#pragma unroll
-              for (int a = 0; a < D; ++a)
-#pragma unroll
-                for (int b = 0; b + a < D; ++b, ++tt) QB[q][tt] = fma(kB[a + b], T[tt], QB[q][tt]);
+              for (int i = 0; i < D; ++i) {
+                UA[q][i] = fma(WA[i], m[i], UA[q][i]);
+                UB[q][i] = fma(WB[i], m[i], UB[q][i]);
+              }
             }
           }
         }
@@ -494,30 +480,24 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
         }
         if (!active) continue;
         if (zA == L - 1) {
-          // ---- window j complete: synthesis at its children, store ----
+          // ---- window j complete: its normal children, store ----
           const int t1 = __ldg(&op.grp1[g1]).z, t2 = __ldg(&op.grp1[j]).z;
           if (t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p) {
             const int4 G0 = __ldg(&op.grp0[fr.g0]);
-            const double* s1 = op.synth1 + g1 * 12;
             const double* s0 = op.synth0 + fr.g0 * 12;
             double* const ob = dst + fr.dst + int64_t(t1 - fr.lo1) * fr.d1 + int64_t(t2 - fr.lo2) * fr.d2 + cb + lane;
 #pragma unroll
-            for (int q = 0; q < NU; ++q) {
-              double R[D];
-              int tt = 0;
+            for (int i = 0; i < 3; ++i) {
+              const int t0 = G0.z + i;
+              if (i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) {
+                double S0[D];
 #pragma unroll
-              for (int a = 0; a < D; ++a) {
-                R[a] = 0.0;
+                for (int a = 0; a < D; ++a) S0[a] = __ldg(s0 + i * 4 + a);
 #pragma unroll
-                for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + b), QA[q][tt], R[a]);
-              }
-#pragma unroll
-              for (int i = 0; i < 3; ++i) {
-                const int t0 = G0.z + i;
-                if (i < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) {
+                for (int q = 0; q < NU; ++q) {
                   double o = 0.0;
 #pragma unroll
-                  for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
+                  for (int a = 0; a < D; ++a) o = fma(S0[a], UA[q][a], o);
                   if (ok[q]) {
                     ob[int64_t(t0 - fr.lo0) * fr.dn + 32 * q] = o;
                     bad |= !isfinite(o);
@@ -529,13 +509,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 #pragma unroll
           for (int q = 0; q < NU; ++q)
 #pragma unroll
-            for (int i = 0; i < NT; ++i) {
-              QA[q][i] = QB[q][i];
-              QB[q][i] = 0.0;
+            for (int i = 0; i < D; ++i) {
+              UA[q][i] = UB[q][i];
+              UB[q][i] = 0.0;
             }
           ++j;
           wA = wB;
+          cA = cB;
           wB = j + 1 < G1 ? __ldg(&op.grp1[j + 1]).x : INT_MAX / 2;
+          cB = j + 1 < G1 ? __ldg(&op.st_cls[j + 1]) : 0;
         }
       }
       if (active) raise_flag(flag, bad);

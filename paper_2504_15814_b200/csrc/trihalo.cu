@@ -11,6 +11,7 @@
 // six face orientations; the orientation only changes strides).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdint>
@@ -66,6 +67,11 @@ struct DevOp {
   int32_t seg_g[3][2];
   int32_t half_g[3][2];
   int32_t half_t[3][2];
+  // staged order3 restriction (stage_slide.cuh): synthesis-row class of every tangential
+  // group and the folded tangential weights W[c1][c2][z][y][a] of every class pair
+  const int32_t* st_cls;
+  const double* st_w;
+  int32_t st_ncls;
 };
 
 // one face, rewritten in reference-frame terms: source cell (a0, a1, a2) of
@@ -374,8 +380,10 @@ struct th_operator {
   // restriction register kernel: mode (0 = not eligible), window, classes, params blob
   int r_mode = 0, r_L = 0, r_ncls = 0;
   std::vector<unsigned char> r_params;
-  // staged order3 restriction (stage_slide.cuh) eligibility
+  // staged order3 restriction (stage_slide.cuh) eligibility and its folded weights
   bool st_ok = false;
+  std::vector<int32_t> st_cls;
+  std::vector<double> st_w;
 };
 
 namespace {
@@ -447,6 +455,45 @@ void prepare_stage(th_operator* op) {
     if (j > 0 && g1[j].win0 < g1[j - 1].win0) return;
     if (j + 2 < g1.size() && g1[j + 2].win0 < g1[j].win0 + 5) return;
   }
+  // Fold the tangential synthesis into per-window weights.  With one t1 child and one t2
+  // child per window the order3 LS value is
+  //   out_i = sum_a S0_i[a] U_a,   U_a = sum_{y,z} W_a(y, z) m_a(y, z),
+  //   W_a(y, z) = sum_{b + c <= 3 - a} S1[b] P_b(y) S2[c] P_c(z)
+  // (m_a = normal Gram moment of source line (y, z)); W depends only on the windows' synthesis
+  // rows, i.e. on the (t1, t2) pair of row classes: interior windows share one row, clipped edge
+  // windows have their own.
+  const int G = (int)g1.size();
+  std::vector<int> rep;  // first group of each class
+  op->st_cls.assign(G, 0);
+  for (int g = 0; g < G; ++g) {
+    int c = 0;
+    for (; c < (int)rep.size(); ++c)
+      if (std::equal(h.synth[1].begin() + g * 12, h.synth[1].begin() + g * 12 + 4,
+                     h.synth[1].begin() + rep[c] * 12))
+        break;
+    if (c == (int)rep.size()) rep.push_back(g);
+    op->st_cls[g] = c;
+  }
+  const int nc = (int)rep.size();
+  if (nc > 6) return;  // > 29 KB of weights: keep the generic slide
+  auto P = [](int d, int x) -> double {  // 5-point Gram polynomials (window.cuh Gram<5>)
+    const int t = x - 2;
+    return d == 0 ? 1.0 : d == 1 ? double(t) : d == 2 ? double(t * t - 2) : double(5 * t * t * t - 17 * t) / 6.0;
+  };
+  op->st_w.assign(size_t(nc) * nc * 100, 0.0);
+  for (int c1 = 0; c1 < nc; ++c1)
+    for (int c2 = 0; c2 < nc; ++c2) {
+      const double* S1 = &h.synth[1][rep[c1] * 12];
+      const double* S2 = &h.synth[1][rep[c2] * 12];
+      for (int z = 0; z < 5; ++z)
+        for (int y = 0; y < 5; ++y)
+          for (int a = 0; a < 4; ++a) {
+            double w = 0.0;
+            for (int b = 0; a + b < 4; ++b)
+              for (int c = 0; a + b + c < 4; ++c) w += S1[b] * P(b, y) * S2[c] * P(c, z);
+            op->st_w[(size_t(c1 * nc + c2) * 25 + z * 5 + y) * 4 + a] = w;
+          }
+    }
   op->st_ok = true;
 }
 
@@ -497,7 +544,7 @@ bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
     }
   g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
   const int NT = h.scheme == TH_SCHEME_TENSOR_LINEAR ? 9 : (L == 3 ? 6 : 10);
-  const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : size_t(g1.size()) * L * 4 * 8;
+  const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : op->st_w.size() * 8;
   // interpolation output staging (TMA bulk stores of contiguous target runs): one block row of
   // <= 3 normal x 3 tg t1 x 3 t2 children; TH_STAGE_OUT=0 disables (direct stores)
   static const int stage_out = [] { const char* e = std::getenv("TH_STAGE_OUT"); return e ? std::atoi(e) : 1; }();
@@ -626,10 +673,12 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
       (rc = upload(op, h.weights, &d.weights)) || (rc = upload(op, h.row_off[0], &d.row_off0)) ||
       (rc = upload(op, h.rows[0], &d.rows0)) || (rc = upload(op, h.row_off[1], &d.row_off1)) ||
       (rc = upload(op, h.rows[1], &d.rows1)) || (rc = upload(op, h.synth[0], &d.synth0)) ||
-      (rc = upload(op, h.synth[1], &d.synth1))) {
+      (rc = upload(op, h.synth[1], &d.synth1)) || (rc = upload(op, op->st_cls, &d.st_cls)) ||
+      (rc = upload(op, op->st_w, &d.st_w))) {
     th_operator_destroy(op);
     return rc;
   }
+  d.st_ncls = op->st_ok ? (int32_t)std::lround(std::sqrt(double(op->st_w.size() / 100))) : 0;
   *out = op;
   return TH_OK;
 }
