@@ -336,3 +336,45 @@ def test_alternative_kernel_paths(th, env):
          "-k", "exchange_all_faces_small or pool_interp_batch or pool_restrict_batch or transposed"],
         env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("u", (1, 33, 65, 130))
+@pytest.mark.parametrize("p", (9, 17))
+def test_pool_restrict_order3_unknown_counts(th, u, p):
+    """Staged order3 restriction across unknown counts: 1 (mostly idle lanes), 33 / 65 (ragged
+    chunks), 130 (3 chunks of 64 -> tiles of 3 t1 groups, several tiles per face)."""
+    import torch
+
+    k = 3
+    rng = np.random.default_rng(u * 10 + p)
+    E = p + 2 * k
+    n_patch, n_face = 10, 6
+    pool = rng.standard_normal((n_patch, E ** 3 * u))
+    nrm = np.arange(n_face) % 3
+    sid = (np.arange(n_face) // 3) % 2
+    fine = rng.integers(0, n_patch, (n_face, 9))
+    rec = th.pool_restrict_faces(p, k, u, fine, nrm, sid)
+    op = th.operators.DEFAULT_CACHE.device_operator("restrict", "order3", p, k)
+    dev = torch.device("cuda")
+    dst = torch.full((n_face * k * p * p * u,), np.nan, dtype=torch.float64, device=dev)
+    th.FaceBatch(op, rec, u).launch(torch.from_numpy(pool.reshape(-1)).to(dev), dst)
+    out = dst.cpu().numpy().reshape(n_face, -1)
+    for f in range(n_face):
+        n = int(nrm[f])
+        t1, t2 = [d for d in range(3) if d != n]
+        ext = [3 * p, 3 * p, 3 * p]
+        ext[n] = 2 * k
+        world = np.zeros((ext[2], ext[1], ext[0], u))
+        for b in range(9):
+            b1, b2 = b % 3, b // 3
+            lo = [k, k, k]
+            lo[n] = 0 if sid[f] == 0 else p
+            e = [p, p, p]
+            e[n] = 2 * k
+            blk = _world_box(pool, E, u, int(fine[f, b]), lo, e).reshape(e[2], e[1], e[0], u)
+            off = [0, 0, 0]
+            off[t1], off[t2] = b1 * p, b2 * p
+            world[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = blk
+        cfg = th.FaceConfig("xyz"[n], ("negative", "positive")[sid[f]], 0, p, k, u)
+        want = oracle_run(cfg, "order3", "restrict", None, world.reshape(-1))
+        assert rel(out[f], want) <= TOL, (u, p, f, rel(out[f], want))
