@@ -105,9 +105,17 @@ def _corner(normal, n_start, t_start, strides):
 
 
 def pool_interp_faces(p: int, k: int, u: int, coarse_ids, normals, sides, segments,
-                      dst_offsets=None) -> np.ndarray:
-    """Interpolation faces reading the coarse patch pool; targets are per-face slabs
-    (k x p x p fine cells in world order, the reference output layout)."""
+                      dst_offsets=None, fine_ids=None) -> np.ndarray:
+    """Interpolation faces reading the coarse patch pool.
+
+    Targets are per-face slabs (k x p x p fine cells in world order, the reference output
+    layout) unless ``fine_ids`` (the fine patch of each face's segment) is given: then the
+    values are written into the pool at the reference's target cells, which are fine patch
+    F's first k interior layers next to the coarse patch — normal [k, 2k) when the coarse
+    side is "negative", [p, p + k) when "positive" — by F's tangential interior (SURVEY A13,
+    geometry.py:202-265).  Those cells are also restriction inputs, so launch this after any
+    restriction that reads them (stream order).
+    """
     normals = np.asarray(normals, dtype=np.int64).ravel()
     sides = np.asarray(sides, dtype=np.int64).ravel()
     coarse_ids = np.asarray(coarse_ids, dtype=np.int64).ravel()
@@ -118,8 +126,13 @@ def pool_interp_faces(p: int, k: int, u: int, coarse_ids, normals, sides, segmen
     n_start = np.where(sides == 0, p, 0)
     rec["src"][:, 0] = coarse_ids * patch + _corner(normals, n_start, k, strides)
     rec["src_stride"] = strides
-    rec["dst_stride"] = world_box_strides(normals, k, p, u)
-    rec["dst"] = np.arange(n, dtype=np.int64) * k * p * p * u if dst_offsets is None else dst_offsets
+    if fine_ids is None:
+        rec["dst_stride"] = world_box_strides(normals, k, p, u)
+        rec["dst"] = np.arange(n, dtype=np.int64) * k * p * p * u if dst_offsets is None else dst_offsets
+    else:
+        fine_ids = np.asarray(fine_ids, dtype=np.int64).ravel()
+        rec["dst_stride"] = strides
+        rec["dst"] = fine_ids * patch + _corner(normals, np.where(sides == 0, k, p), k, strides)
     return rec
 
 

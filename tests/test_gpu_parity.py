@@ -378,3 +378,36 @@ def test_pool_restrict_order3_unknown_counts(th, u, p):
         cfg = th.FaceConfig("xyz"[n], ("negative", "positive")[sid[f]], 0, p, k, u)
         want = oracle_run(cfg, "order3", "restrict", None, world.reshape(-1))
         assert rel(out[f], want) <= TOL, (u, p, f, rel(out[f], want))
+
+
+@pytest.mark.parametrize("scheme", ("tensor_linear", "order2", "order3"))
+def test_interp_into_fine_patches(th, scheme):
+    """Interpolation written into the fine patches' reference target cells equals the slab run."""
+    import torch
+
+    p, k, u = 9, 3, 7
+    rng = np.random.default_rng(5)
+    E = p + 2 * k
+    n_face = 12
+    coarse = rng.standard_normal((4, E ** 3 * u))
+    fine = np.zeros((n_face, E ** 3 * u))
+    cid = rng.integers(0, 4, n_face)
+    nrm, sid, seg = np.arange(n_face) % 3, (np.arange(n_face) // 3) % 2, rng.integers(0, 9, n_face)
+    dev = torch.device("cuda")
+    op = th.operators.DEFAULT_CACHE.device_operator("interpolate", scheme, p, k)
+    src = torch.from_numpy(coarse.reshape(-1)).to(dev)
+    slab = torch.zeros(n_face * k * p * p * u, dtype=torch.float64, device=dev)
+    th.FaceBatch(op, th.pool_interp_faces(p, k, u, cid, nrm, sid, seg), u).launch(src, slab)
+    fdst = torch.from_numpy(fine.reshape(-1)).to(dev)
+    rec = th.pool_interp_faces(p, k, u, cid, nrm, sid, seg, fine_ids=np.arange(n_face))
+    th.FaceBatch(op, rec, u).launch(src, fdst)
+    slab = slab.cpu().numpy().reshape(n_face, -1)
+    fp = fdst.cpu().numpy().reshape(n_face, E, E, E, u)
+    for f in range(n_face):
+        lo, ext = [k, k, k], [p, p, p]
+        lo[nrm[f]] = k if sid[f] == 0 else p
+        ext[nrm[f]] = k
+        box = fp[f, lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]].reshape(-1)
+        assert np.array_equal(box, slab[f])
+        fp[f, lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]] = 0.0
+    assert not fp.any()  # nothing written outside the target boxes
