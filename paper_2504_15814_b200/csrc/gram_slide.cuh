@@ -181,14 +181,20 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
 #pragma unroll
             for (int t = 0; t < NT; ++t) o[t] = fma(w, slot[t * 32], o[t]);
           }
+          if (ok) {  // one lane-divergent region per t2 child (not one per store)
+            double* const dl = dbase + do2;
 #pragma unroll
-          for (int j = 0; j < CT; ++j)
+            for (int j = 0; j < CT; ++j) {
+              if (!ok1[j]) continue;
+              double* const dj = dl + do1[j];
 #pragma unroll
-            for (int i = 0; i < C0; ++i)
-              if (ok1[j] && ok0[i] && ok) {
-                dbase[do0[i] + do1[j] + do2] = o[i + C0 * j];
-                bad |= !isfinite(o[i + C0 * j]);
-              }
+              for (int i = 0; i < C0; ++i)
+                if (ok0[i]) {
+                  dj[do0[i]] = o[i + C0 * j];
+                  bad |= !isfinite(o[i + C0 * j]);
+                }
+            }
+          }
         }
         raise_flag(flag, bad);
         continue;
@@ -217,10 +223,10 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
       bool bad = false;
       double* const dbase = dst + fr.dst + cb + lane;
 #pragma unroll
-      for (int l = 0; l < CT; ++l) {
+      for (int l = 0; l < CT && ok; ++l) {  // lanes past u skip the synthesis: one divergent region
         const int tz = G2.z + l;
         if (!(l < G2.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
-        const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
+        double* const dl = dbase + int64_t(tz - fr.lo2) * fr.d2;
         double Q[NT];
         int t = 0, mi = 0;
 #pragma unroll
@@ -242,16 +248,15 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
 #pragma unroll
             for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + j * 4 + b), Q[tt], R[a]);
           }
+          double* const dj = dl + do1[j];
 #pragma unroll
           for (int i = 0; i < C0; ++i) {
             if (!ok0[i]) continue;
             double o = 0.0;
 #pragma unroll
             for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
-            if (ok) {
-              dbase[do0[i] + do1[j] + do2] = o;
-              bad |= !isfinite(o);
-            }
+            dj[do0[i]] = o;
+            bad |= !isfinite(o);
           }
         }
       }
