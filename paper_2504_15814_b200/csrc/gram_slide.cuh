@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         bool bad = false;
         double* const dbase = dst + fr.dst + cb + lane;
 #pragma unroll
-        for (int l = 0; l < CT; ++l) {
+        for (int l = 0; l < CT && ok; ++l) {  // lanes past u skip the z-pass and stores
           const int tz = G2.z + l;
           if (!(l < G2.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
           const int64_t do2 = int64_t(tz - fr.lo2) * fr.d2;
@@ -181,19 +181,17 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
 #pragma unroll
             for (int t = 0; t < NT; ++t) o[t] = fma(w, slot[t * 32], o[t]);
           }
-          if (ok) {  // one lane-divergent region per t2 child (not one per store)
-            double* const dl = dbase + do2;
+          double* const dl = dbase + do2;
 #pragma unroll
-            for (int j = 0; j < CT; ++j) {
-              if (!ok1[j]) continue;
-              double* const dj = dl + do1[j];
+          for (int j = 0; j < CT; ++j) {
+            if (!ok1[j]) continue;
+            double* const dj = dl + do1[j];
 #pragma unroll
-              for (int i = 0; i < C0; ++i)
-                if (ok0[i]) {
-                  dj[do0[i]] = o[i + C0 * j];
-                  bad |= !isfinite(o[i + C0 * j]);
-                }
-            }
+            for (int i = 0; i < C0; ++i)
+              if (ok0[i]) {
+                dj[do0[i]] = o[i + C0 * j];
+                bad |= !isfinite(o[i + C0 * j]);
+              }
           }
         }
         raise_flag(flag, bad);
