@@ -119,43 +119,45 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         const int64_t zo = int64_t(a2 - b2 * p) * fr.s2;
         // (no prefetch of the next slice: TMA bulk and per-line L2 prefetches both measured
         //  slower here, and indexing ybase[] at run time would push it to local memory)
-        double v[L][L];
-#pragma unroll
-        for (int y = 0; y < L; ++y) {
-          // interpolation rows are affine in y (one base + y * s1, fewer live registers);
-          // restriction rows may cross a fine-block boundary, so they use the per-row table
-          const int64_t base = ROLE == 0 ? ibase + zo + int64_t(y) * fr.s1
-                                         : ybase[y] + zo + __ldg(&fp->src[yb[y] + 3 * b2]);
-#pragma unroll
-          for (int x = 0; x < L; ++x) v[y][x] = ok ? ldg_slice(src + base + int64_t(x) * fr.sn) : 0.0;
-        }
-        double T[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) T[t] = 0.0;
-#pragma unroll
-        for (int y = 0; y < L; ++y) {
-          if constexpr (TENSOR) {
-#pragma unroll
-            for (int c0 = 0; c0 < C0; ++c0) {
-              double tx = 0.0;
-#pragma unroll
-              for (int x = 0; x < L; ++x) tx = fma(R0[c0][x], v[y][x], tx);
-#pragma unroll
-              for (int c1 = 0; c1 < CT; ++c1) T[c0 + C0 * c1] = fma(R1[c1][y], tx, T[c0 + C0 * c1]);
-            }
-          } else {
-            double m[D];
-            gram_moments<L, D>(v[y], m);
-            int t = 0;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-              for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
+        if (ok) {  // lanes past u skip the slice (one divergent region, no per-load predicate)
+          double v[L][L];
+  #pragma unroll
+          for (int y = 0; y < L; ++y) {
+            // interpolation rows are affine in y (one base + y * s1, fewer live registers);
+            // restriction rows may cross a fine-block boundary, so they use the per-row table
+            const int64_t base = ROLE == 0 ? ibase + zo + int64_t(y) * fr.s1
+                                           : ybase[y] + zo + __ldg(&fp->src[yb[y] + 3 * b2]);
+  #pragma unroll
+            for (int x = 0; x < L; ++x) v[y][x] = ldg_slice(src + base + int64_t(x) * fr.sn);
           }
+          double T[NT];
+  #pragma unroll
+          for (int t = 0; t < NT; ++t) T[t] = 0.0;
+  #pragma unroll
+          for (int y = 0; y < L; ++y) {
+            if constexpr (TENSOR) {
+  #pragma unroll
+              for (int c0 = 0; c0 < C0; ++c0) {
+                double tx = 0.0;
+  #pragma unroll
+                for (int x = 0; x < L; ++x) tx = fma(R0[c0][x], v[y][x], tx);
+  #pragma unroll
+                for (int c1 = 0; c1 < CT; ++c1) T[c0 + C0 * c1] = fma(R1[c1][y], tx, T[c0 + C0 * c1]);
+              }
+            } else {
+              double m[D];
+              gram_moments<L, D>(v[y], m);
+              int t = 0;
+  #pragma unroll
+              for (int a = 0; a < D; ++a)
+  #pragma unroll
+                for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
+            }
+          }
+          double* slot = ring + (a2 % L) * (NT * 32);
+  #pragma unroll
+          for (int t = 0; t < NT; ++t) slot[t * 32] = T[t];
         }
-        double* slot = ring + (a2 % L) * (NT * 32);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) slot[t * 32] = T[t];
         asm volatile("" ::: "memory");  // one slice of loads live at a time
       }
       hi = max(hi, w2 + L - 1);
