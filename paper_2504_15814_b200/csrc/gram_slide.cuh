@@ -199,67 +199,69 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         raise_flag(flag, bad);
         continue;
       }
-      // ---- z-pass of this block -------------------------------------------------
-      double M[NM];
-#pragma unroll
-      for (int i = 0; i < NM; ++i) M[i] = 0.0;
-      int slot0 = w2 % L;
-#pragma unroll
-      for (int z = 0; z < L; ++z) {
-        const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
-        const double* slot = ring + sl * (NT * 32);
-        int t = 0, mi = 0;
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = 0; b + a < D; ++b, ++t) {
-            const double Tz = slot[t * 32];
-#pragma unroll
-            for (int c = 0; c + b + a < D; ++c, ++mi) gacc(M[mi], Gram<L>::P(c, z), Tz);
-          }
-      }
-      // ---- synthesis at the children and store -----------------------------------
-      const double* s2 = op.synth1 + g2 * 12;
+      // ---- z-pass of this block (lanes past u skip it and the synthesis) -----------
       bool bad = false;
-      double* const dbase = dst + fr.dst + cb + lane;
+      if (ok) {
+        double M[NM];
+        const int slot0 = w2 % L;
+        {
+          int t = 0, mi = 0;
 #pragma unroll
-      for (int l = 0; l < CT && ok; ++l) {  // lanes past u skip the synthesis: one divergent region
-        const int tz = G2.z + l;
-        if (!(l < G2.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
-        double* const dl = dbase + int64_t(tz - fr.lo2) * fr.d2;
-        double Q[NT];
-        int t = 0, mi = 0;
+          for (int a = 0; a < D; ++a)
 #pragma unroll
-        for (int a = 0; a < D; ++a)
+            for (int b = 0; b + a < D; ++b, ++t) {
+              double col[L];  // T_ab over the window's slices -> its z moments
 #pragma unroll
-          for (int b = 0; b + a < D; ++b, ++t) {
-            Q[t] = 0.0;
+              for (int z = 0; z < L; ++z) {
+                const int sl = slot0 + z >= L ? slot0 + z - L : slot0 + z;
+                col[z] = ring[sl * (NT * 32) + t * 32];
+              }
+              gram_moments_n<L>(col, M + mi, D - a - b);
+              mi += D - a - b;
+            }
+        }
+        // ---- synthesis at the children and store -----------------------------------
+        const double* s2 = op.synth1 + g2 * 12;
+        double* const dbase = dst + fr.dst + cb + lane;
 #pragma unroll
-            for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(__ldg(s2 + l * 4 + c), M[mi], Q[t]);
-          }
+        for (int l = 0; l < CT; ++l) {
+          const int tz = G2.z + l;
+          if (!(l < G2.w && tz >= fr.lo2 && tz < fr.lo2 + p)) continue;
+          double* const dl = dbase + int64_t(tz - fr.lo2) * fr.d2;
+          double Q[NT];
+          int t = 0, mi = 0;
 #pragma unroll
-        for (int j = 0; j < CT; ++j) {
-          if (!ok1[j]) continue;
-          double R[D];
-          int tt = 0;
+          for (int a = 0; a < D; ++a)
 #pragma unroll
-          for (int a = 0; a < D; ++a) {
-            R[a] = 0.0;
+            for (int b = 0; b + a < D; ++b, ++t) {
+              Q[t] = 0.0;
 #pragma unroll
-            for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + j * 4 + b), Q[tt], R[a]);
-          }
-          double* const dj = dl + do1[j];
+              for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(__ldg(s2 + l * 4 + c), M[mi], Q[t]);
+            }
 #pragma unroll
-          for (int i = 0; i < C0; ++i) {
-            if (!ok0[i]) continue;
-            double o = 0.0;
+          for (int j = 0; j < CT; ++j) {
+            if (!ok1[j]) continue;
+            double R[D];
+            int tt = 0;
 #pragma unroll
-            for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
-            dj[do0[i]] = o;
-            bad |= !isfinite(o);
+            for (int a = 0; a < D; ++a) {
+              R[a] = 0.0;
+#pragma unroll
+              for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + j * 4 + b), Q[tt], R[a]);
+            }
+            double* const dj = dl + do1[j];
+#pragma unroll
+            for (int i = 0; i < C0; ++i) {
+              if (!ok0[i]) continue;
+              double o = 0.0;
+#pragma unroll
+              for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
+              dj[do0[i]] = o;
+              bad |= !isfinite(o);
+            }
           }
         }
-      }
+      }  // ok
       raise_flag(flag, bad);
     }
   }

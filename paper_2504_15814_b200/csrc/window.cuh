@@ -63,6 +63,26 @@ __device__ __forceinline__ void gram_moments(const double (&v)[L], double (&m)[N
   }
 }
 
+// gram_moments with the moment count n given at run time (a constant after unrolling)
+template <int L>
+__device__ __forceinline__ void gram_moments_n(const double (&v)[L], double* m, int n) {
+  if constexpr (L == 5) {
+    const double s04 = v[0] + v[4], s13 = v[1] + v[3];
+    m[0] = (s04 + s13) + v[2];
+    if (n > 1) {
+      const double d40 = v[4] - v[0], d31 = v[3] - v[1];
+      m[1] = fma(2.0, d40, d31);
+      if (n > 2) m[2] = fma(2.0, s04 - v[2], -s13);
+      if (n > 3) m[3] = fma(-2.0, d31, d40);
+    }
+  } else {
+    const double s02 = v[0] + v[2];
+    m[0] = s02 + v[1];
+    if (n > 1) m[1] = v[2] - v[0];
+    if (n > 2) m[2] = fma(-2.0, v[1], s02);
+  }
+}
+
 // y-pass of the per-line x moments mm[y][a]: T_ab = sum_y P_b(y) mm[y][a] for a + b < D,
 // pairs ordered a-major (T index = a D - a(a-1)/2 + b), each column through gram_moments
 template <int L, int D, int A = 0, int NT>
