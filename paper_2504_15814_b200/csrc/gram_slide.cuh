@@ -79,6 +79,13 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
       ok1[i] = i < G1.w && t >= fr.lo1 && t < fr.lo1 + p;
       do1[i] = int64_t(t - fr.lo1) * fr.d1;
     }
+    // every normal / t1 child of this unit is a target (always at p = 9): the stores below
+    // then need no per-child test (warp-uniform, but the compiler cannot know that)
+    bool all01 = true;
+#pragma unroll
+    for (int i = 0; i < C0; ++i) all01 &= ok0[i];
+#pragma unroll
+    for (int i = 0; i < CT; ++i) all01 &= ok1[i];
     const double* s0 = op.synth0 + g0 * 12;
     const double* s1 = op.synth1 + g1 * 12;
     double R0[TENSOR ? C0 : 1][TENSOR ? L : 1], R1[TENSOR ? CT : 1][TENSOR ? L : 1];
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         // ---- z-pass with the t2 rows straight into the children, store --------
         const double* r2 = op.rows1 + __ldg(&op.row_off1[g2]);
         const int slot0 = w2 % L;
-        bool bad = false;
+        double chk = 0.0;  // fma(o, 0, chk) stays 0 for finite o, turns NaN for any Inf / NaN
         double* const dbase = dst + fr.dst + cb + lane;
 #pragma unroll
         for (int l = 0; l < CT && ok; ++l) {  // lanes past u skip the z-pass and stores
@@ -184,23 +191,33 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             for (int t = 0; t < NT; ++t) o[t] = fma(w, slot[t * 32], o[t]);
           }
           double* const dl = dbase + do2;
+          if (all01) {
 #pragma unroll
-          for (int j = 0; j < CT; ++j) {
-            if (!ok1[j]) continue;
-            double* const dj = dl + do1[j];
+            for (int j = 0; j < CT; ++j)
 #pragma unroll
-            for (int i = 0; i < C0; ++i)
-              if (ok0[i]) {
-                dj[do0[i]] = o[i + C0 * j];
-                bad |= !isfinite(o[i + C0 * j]);
+              for (int i = 0; i < C0; ++i) {
+                dl[do1[j] + do0[i]] = o[i + C0 * j];
+                chk = fma(o[i + C0 * j], 0.0, chk);
               }
+          } else {
+#pragma unroll
+            for (int j = 0; j < CT; ++j) {
+              if (!ok1[j]) continue;
+              double* const dj = dl + do1[j];
+#pragma unroll
+              for (int i = 0; i < C0; ++i)
+                if (ok0[i]) {
+                  dj[do0[i]] = o[i + C0 * j];
+                  chk = fma(o[i + C0 * j], 0.0, chk);
+                }
+            }
           }
         }
-        raise_flag(flag, bad);
+        raise_flag(flag, !isfinite(chk));
         continue;
       }
       // ---- z-pass of this block (lanes past u skip it and the synthesis) -----------
-      bool bad = false;
+      double chk = 0.0;  // fma(o, 0, chk) stays 0 for finite o, turns NaN for any Inf / NaN
       if (ok) {
         double M[NM];
         const int slot0 = w2 % L;
@@ -240,7 +257,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             }
 #pragma unroll
           for (int j = 0; j < CT; ++j) {
-            if (!ok1[j]) continue;
+            if (!all01 && !ok1[j]) continue;
             double R[D];
             int tt = 0;
 #pragma unroll
@@ -252,17 +269,17 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             double* const dj = dl + do1[j];
 #pragma unroll
             for (int i = 0; i < C0; ++i) {
-              if (!ok0[i]) continue;
+              if (!all01 && !ok0[i]) continue;
               double o = 0.0;
 #pragma unroll
               for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
               dj[do0[i]] = o;
-              bad |= !isfinite(o);
+              chk = fma(o, 0.0, chk);
             }
           }
         }
       }  // ok
-      raise_flag(flag, bad);
+      raise_flag(flag, !isfinite(chk));
     }
   }
 }
