@@ -36,6 +36,15 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
   extern __shared__ double ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* const ring = ring_all + warp * (L * NT * 32) + lane;  // [slot][t] x 32 lanes, lane-private
+  // synthesis tables of all groups in shared memory (broadcast reads; from global memory their
+  // load latency was ~1/3 of the order3 interpolation's stalls)
+  double* const ssyn0 = ring_all + (blockDim.x >> 5) * (L * NT * 32);
+  double* const ssyn1 = ssyn0 + op.G0 * 12;
+  if constexpr (!TENSOR) {
+    for (int i = threadIdx.x; i < op.G0 * 12; i += blockDim.x) ssyn0[i] = __ldg(op.synth0 + i);
+    for (int i = threadIdx.x; i < op.G1 * 12; i += blockDim.x) ssyn1[i] = __ldg(op.synth1 + i);
+    __syncthreads();
+  }
   const int p = op.p;
   const int upf = op.units_per_face;
   const int nch = (u + 31) / 32;
@@ -86,8 +95,8 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
     for (int i = 0; i < C0; ++i) all01 &= ok0[i];
 #pragma unroll
     for (int i = 0; i < CT; ++i) all01 &= ok1[i];
-    const double* s0 = op.synth0 + g0 * 12;
-    const double* s1 = op.synth1 + g1 * 12;
+    const double* s0 = ssyn0 + g0 * 12;
+    const double* s1 = ssyn1 + g1 * 12;
     double R0[TENSOR ? C0 : 1][TENSOR ? L : 1], R1[TENSOR ? CT : 1][TENSOR ? L : 1];
     if constexpr (TENSOR) {
       const double* r0 = op.rows0 + __ldg(&op.row_off0[g0]);
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             }
         }
         // ---- synthesis at the children and store -----------------------------------
-        const double* s2 = op.synth1 + g2 * 12;
+        const double* s2 = ssyn1 + g2 * 12;
         double* const dbase = dst + fr.dst + cb + lane;
 #pragma unroll
         for (int l = 0; l < CT; ++l) {
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             for (int b = 0; b + a < D; ++b, ++t) {
               Q[t] = 0.0;
 #pragma unroll
-              for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(__ldg(s2 + l * 4 + c), M[mi], Q[t]);
+              for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(s2[l * 4 + c], M[mi], Q[t]);
             }
 #pragma unroll
           for (int j = 0; j < CT; ++j) {
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
             for (int a = 0; a < D; ++a) {
               R[a] = 0.0;
 #pragma unroll
-              for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(__ldg(s1 + j * 4 + b), Q[tt], R[a]);
+              for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(s1[j * 4 + b], Q[tt], R[a]);
             }
             double* const dj = dl + do1[j];
 #pragma unroll
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
               if (!all01 && !ok0[i]) continue;
               double o = 0.0;
 #pragma unroll
-              for (int a = 0; a < D; ++a) o = fma(__ldg(s0 + i * 4 + a), R[a], o);
+              for (int a = 0; a < D; ++a) o = fma(s0[i * 4 + a], R[a], o);
               dj[do0[i]] = o;
               chk = fma(o, 0.0, chk);
             }

@@ -762,7 +762,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
 #define TH_GRAM(ORDER, ROLE, MINB)                                                                     \
   do {                                                                                                 \
     auto kfn = gram_slide_kernel<ORDER, ROLE, MINB>;                                                   \
-    const size_t smem = size_t(4) * (ORDER == 2 ? 3 * 6 : 5 * 10) * 32 * 8;                            \
+    const size_t smem = size_t(4) * (ORDER == 2 ? 3 * 6 : 5 * 10) * 32 * 8 +                           \
+                        size_t(op->dev.G0 + op->dev.G1) * 12 * 8;                                      \
     if (smem > 48 * 1024) TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
     const int64_t units = n_faces * int64_t(op->dev.units_per_face) * ((u + 31) / 32);                 \
     const int gblocks = int(std::min<int64_t>((units + 3) / 4, int64_t(num_sms()) * MINB * 2));       \
