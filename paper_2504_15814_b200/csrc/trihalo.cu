@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "restrict_pipe.cuh"
 #include "gram_slide.cuh"
 #include "stage_slide.cuh"
+#include "tile_interp.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -384,6 +385,9 @@ struct th_operator {
   bool st_ok = false;
   std::vector<int32_t> st_cls;
   std::vector<double> st_w;
+  // staged tile interpolation (tile_interp.cuh): mode (0 = not eligible, 1 = tensor_linear,
+  // 2 = order2 Gram) and tiles per face axis
+  int ti_mode = 0, ti_nt = 0;
 };
 
 namespace {
@@ -495,6 +499,45 @@ void prepare_stage(th_operator* op) {
           }
     }
   op->st_ok = true;
+}
+
+// Staged tile interpolation eligibility (tile_interp.cuh): one normal group with a 3-cell
+// window and <= 3 children; tangential groups with 3-cell windows, <= 3 children and
+// non-decreasing starts.  A face axis splits into ti_nt balanced tiles of <= 3 groups whose
+// windows span <= TNY cells (the shared-memory box).
+void prepare_tile(th_operator* op) {
+  const th::HostOperator& h = op->host;
+  op->ti_mode = 0;
+  if (h.role != 0 || h.groups[0].size() != 1 || h.groups[1].empty()) return;
+  int mode = 0;
+  if (h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) mode = 1;
+  else if (h.gram_ok && h.fast_C0 == 3 && h.scheme == TH_SCHEME_ORDER2 && !h.synth[1].empty()) mode = 2;
+  if (!mode) return;
+  const th::Group& g0 = h.groups[0][0];
+  if (g0.winL != 3 || g0.tgtN < 1 || g0.tgtN > 3) return;
+  const auto& g1 = h.groups[1];
+  for (size_t j = 0; j < g1.size(); ++j) {
+    if (g1[j].winL != 3 || g1[j].tgtN < 1 || g1[j].tgtN > 3) return;
+    if (j > 0 && g1[j].win0 < g1[j - 1].win0) return;
+  }
+  int nmax = 0;
+  for (int c = 0; c < 3; ++c) nmax = std::max(nmax, h.seg_g[c][1] - h.seg_g[c][0]);
+  if (nmax < 1) return;
+  const int nt = (nmax + 2) / 3;
+  for (int c = 0; c < 3; ++c) {
+    const int n = h.seg_g[c][1] - h.seg_g[c][0];
+    for (int t = 0; t < nt; ++t) {
+      const int a = t * n / nt, b = (t + 1) * n / nt;
+      if (b - a > 3) return;
+      if (b > a && g1[h.seg_g[c][0] + b - 1].win0 + 3 - g1[h.seg_g[c][0] + a].win0 > TNY) return;
+    }
+  }
+  // one tile per face only: at p = 17 (3 x 3 tiles of partial blocks) the per-warp slide is
+  // faster (config 4 order2 interpolation 0.56 vs 0.43-0.49 of HBM, profiles/r01_ab_tile.txt)
+  static const bool multi = [] { const char* e = std::getenv("TH_TILE_MULTI"); return e && std::atoi(e); }();
+  if (nt > 1 && !multi) return;
+  op->ti_mode = mode;
+  op->ti_nt = nt;
 }
 
 // launch geometry of the slice-staged kernels (stage_slide.cuh) for u unknowns;
@@ -663,6 +706,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   if (op->smem_bytes > 200 * 1024) op->smem_ok = false;
   prepare_restrict(op);
   prepare_stage(op);
+  prepare_tile(op);
   if (!upload_to_device) {
     *out = op;
     return TH_OK;
@@ -793,6 +837,44 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   static const int stage_interp = [] { const char* e = std::getenv("TH_STAGE_INTERP"); return e ? std::atoi(e) : 0; }();
   const bool gram = h.gram_ok && h.fast_C0 == 3;
   const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
+  //   TH_TILE=0                  per-warp slide (gram_slide.cuh) instead of the tile-parallel
+  //                              interpolation kernel (tile_interp.cuh)
+  static const int use_tile = [] { const char* e = std::getenv("TH_TILE"); return e ? std::atoi(e) : 1; }();
+  if (use_tile && interp && op->ti_mode && !stage_interp) {
+    const int nt = op->ti_nt;
+    const int pitch = TBOX | 1;
+    const int TW = op->ti_mode == 1 ? 9 : 12;
+    const size_t smem = 8 * (size_t(tile_box_offset(TW, op->dev.G0, op->dev.G1)) + size_t(2) * u * pitch);
+    // exact unknown split of the flattened item index (idx < 9 u) through a 32-bit reciprocal
+    const bool exact = uint64_t(9) * u * uint64_t(u) < (uint64_t(1) << 32);
+    if (smem <= 220 * 1024 && exact) {
+      const unsigned umag = unsigned((uint64_t(1) << 32) / unsigned(u) + 1);
+      const int64_t tiles = n_faces * int64_t(nt) * nt;
+#define TH_TILEK(TENSOR, NTH, MINB)                                                                         \
+  do {                                                                                                      \
+    auto kfn = tile_interp_kernel<TENSOR, NTH, MINB>;                                                       \
+    if (smem > 48 * 1024) TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
+    int per_sm = 0;                                                                                         \
+    TH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NTH, smem));                       \
+    const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));          \
+    kfn<<<tblocks, NTH, smem, s>>>(op->dev, src, dst, faces, tiles, nt, pitch, u, umag, flag);              \
+  } while (0)
+      // TH_TILE_CFG (A/B): 0 = 192 threads x 2 CTAs/SM (default), 1 = 192 x 3, 2 = 256 x 2
+      static const int tcfg = [] { const char* e = std::getenv("TH_TILE_CFG"); return e ? std::atoi(e) : 0; }();
+      if (op->ti_mode == 1) {
+        if (tcfg == 1) TH_TILEK(true, 192, 3);
+        else if (tcfg == 2) TH_TILEK(true, 256, 2);
+        else TH_TILEK(true, 192, 2);
+      } else {
+        if (tcfg == 1) TH_TILEK(false, 192, 3);
+        else if (tcfg == 2) TH_TILEK(false, 256, 2);
+        else TH_TILEK(false, 192, 2);
+      }
+#undef TH_TILEK
+      TH_CUDA(cudaGetLastError());
+      return TH_OK;
+    }
+  }
   StageGeom sg;
   if (stage_interp && interp && stage_geometry(op, u, h.scheme == TH_SCHEME_ORDER3 ? 1 : 2, sg)) {
     if (h.scheme == TH_SCHEME_ORDER3) TH_SLIDE(0, 3, false, kInterpNCW, 1, 1);

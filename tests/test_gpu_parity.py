@@ -321,11 +321,14 @@ def test_pool_transposed_layout(th, scheme, p):
         assert np.array_equal(outs[0], outs[1]), (role, scheme, np.abs(outs[0] - outs[1]).max())
 
 
-@pytest.mark.parametrize("env", ({"TH_STAGE_INTERP": "1"}, {"TH_GRAM": "3"}))
+@pytest.mark.parametrize("env", ({"TH_STAGE_INTERP": "1"}, {"TH_GRAM": "3"}, {"TH_TILE": "0"},
+                                 {"TH_TILE_MULTI": "1"}, {"TH_TILE_CFG": "2"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
     parity tests in a child process with the alternative paths (slice-staged
-    interpolation; the per-warp order3 restriction slide)."""
+    interpolation; the per-warp order3 restriction slide; the per-warp interpolation
+    slide instead of the staged tile kernel; staged tiles also at p = 17, where a face
+    splits into 3 x 3 tiles of partial blocks; another tile CTA shape)."""
     import os
     import subprocess
     import sys
@@ -411,3 +414,65 @@ def test_interp_into_fine_patches(th, scheme):
         assert np.array_equal(box, slab[f])
         fp[f, lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]] = 0.0
     assert not fp.any()  # nothing written outside the target boxes
+
+
+@pytest.mark.parametrize("scheme", ("tensor_linear", "order2", "order3"))
+def test_interp_wide_target_strides(th, scheme):
+    """Target strides beyond 2^21 elements take the kernels' 64-bit offset path; the values
+    must equal those written through compact slabs bit for bit."""
+    import torch
+
+    p, k, u = 9, 3, 59
+    rng = np.random.default_rng(77)
+    E = p + 2 * k
+    n_patch, n_face = 4, 3
+    pool = torch.from_numpy(rng.standard_normal(n_patch * E ** 3 * u)).to("cuda")
+    nrm, sid, seg = np.array([0, 1, 2]), np.array([0, 1, 0]), np.array([4, 0, 8])
+    rec = th.pool_interp_faces(p, k, u, rng.integers(0, n_patch, n_face), nrm, sid, seg)
+    op = th.operators.DEFAULT_CACHE.device_operator("interpolate", scheme, p, k)
+    ncell = k * p * p
+    dst = torch.full((n_face * ncell * u,), np.nan, dtype=torch.float64, device="cuda")
+    th.FaceBatch(op, rec, u).launch(pool, dst)
+    want = dst.cpu().numpy().reshape(n_face, ncell * u)
+    wide = rec.copy()
+    # t1 / z strides spread out, z beyond 2^21 elements for every face
+    scale = np.ones((n_face, 3), dtype=np.int64)
+    scale[:, 1] = 7
+    scale[:, 2] = 2 ** 21 // rec["dst_stride"][:, 2] + 1
+    wide["dst_stride"] = rec["dst_stride"] * scale
+    span = int((wide["dst_stride"] * (np.where(np.arange(3)[None, :] == nrm[:, None], k, p) - 1)).sum(1).max()) + u
+    wide["dst"] = np.arange(n_face, dtype=np.int64) * span
+    assert (wide["dst_stride"].max(1) >= 2 ** 21).all()
+    big = torch.full((n_face * span,), np.nan, dtype=torch.float64, device="cuda")
+    th.FaceBatch(op, wide, u).launch(pool, big)
+    big = big.cpu().numpy()
+    for f in range(n_face):
+        ext = np.where(np.arange(3) == nrm[f], k, p)
+        c = np.arange(ncell)
+        x, y, z = c % ext[0], (c // ext[0]) % ext[1], c // (ext[0] * ext[1])
+        base = wide["dst"][f] + x * wide["dst_stride"][f, 0] + y * wide["dst_stride"][f, 1] + z * wide["dst_stride"][f, 2]
+        got = big[(base[:, None] + np.arange(u)[None, :]).reshape(-1)]
+        assert np.array_equal(got, want[f]), (scheme, f)
+
+
+@pytest.mark.parametrize("scheme", ("tensor_linear", "order2", "order3"))
+def test_interp_batch_nonfinite_flag(th, scheme):
+    """A NaN / Inf inside a face's support raises the batch's non-finite flag (every
+    interpolation kernel: staged tiles, per-warp slide); a finite pool does not."""
+    import torch
+
+    p, k, u = 9, 3, 59
+    E = p + 2 * k
+    op = th.operators.DEFAULT_CACHE.device_operator("interpolate", scheme, p, k)
+    rec = th.pool_interp_faces(p, k, u, [1, 0], [2, 0], [0, 1], [4, 0])
+    batch = th.FaceBatch(op, rec, u)
+    src = torch.zeros(2 * E ** 3 * u, dtype=torch.float64, device="cuda")
+    out = torch.empty(2 * k * p * p * u, dtype=torch.float64, device="cuda")
+    batch.launch(src, out)
+    assert not batch.nonfinite()
+    for bad in (float("nan"), float("inf")):
+        src.zero_()
+        # coarse patch 1, normal z, side 0: support layers [p, p + 2k) around segment 4's cells
+        src.view(2, E, E, E, u)[1, p + 2, k + 4, k + 4, 58] = bad
+        batch.launch(src, out)
+        assert batch.nonfinite(), (scheme, bad)
