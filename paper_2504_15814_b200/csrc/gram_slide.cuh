@@ -47,6 +47,10 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
   }
   const int p = op.p;
   const int upf = op.units_per_face;
+  // finiteness of the inputs: every value of a source slice enters its T[0] (Gram: the plain
+  // sum; tensor: an fma chain through all of them), so fma(T0, 0, chk) turns NaN for any
+  // Inf / NaN in the support and stays 0 otherwise (checked once, at the end)
+  double chk = 0.0;
   const int nch = (u + 31) / 32;
   const int64_t total = n_faces * upf * nch;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -117,11 +121,13 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
       //  next unit as well measured slower: profiles/r01_ab_stage.txt)
       const int z0 = __ldg(&op.grp1[fr.g2]).x, nz = __ldg(&op.grp1[fr.g2 + fr.n2 - 1]).x + L - z0;
       const char* const c0 = reinterpret_cast<const char*>(src + (ibase - lane + int64_t(z0) * fr.s2));
-      for (int i = lane; i < L * L * nz * 3; i += 32) {
-        const int cell = i / 3, part = i - cell * 3;
-        const int x = cell % L, y = (cell / L) % L, z = cell / (L * L);
-        l2_prefetch_line(c0 + 8 * (int64_t(x) * fr.sn + int64_t(y) * fr.s1 + int64_t(z) * fr.s2) +
-                         (part == 2 ? 255 : part * 128));
+      // a cell per lane and iteration, its <= 3 lines of this chunk (256 bytes at 8-byte alignment)
+      for (int c = lane; c < L * L * nz; c += 32) {
+        const int x = c % L, yz = c / L, y = yz % L, z = yz / L;
+        const char* const pc = c0 + 8 * (int64_t(x) * fr.sn + int64_t(y) * fr.s1 + int64_t(z) * fr.s2);
+        l2_prefetch_line(pc);
+        l2_prefetch_line(pc + 128);
+        l2_prefetch_line(pc + 255);
       }
     }
     int hi = -1;  // highest t2 source slice held in the ring
@@ -170,6 +176,7 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
                 for (int b = 0; b + a < D; ++b, ++t) gacc(T[t], Gram<L>::P(b, y), m[a]);
             }
           }
+          chk = fma(T[0], 0.0, chk);
           double* slot = ring + (a2 % L) * (NT * 32);
   #pragma unroll
           for (int t = 0; t < NT; ++t) slot[t * 32] = T[t];
@@ -181,7 +188,6 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
         // ---- z-pass with the t2 rows straight into the children, store --------
         const double* r2 = op.rows1 + __ldg(&op.row_off1[g2]);
         const int slot0 = w2 % L;
-        double chk = 0.0;  // fma(o, 0, chk) stays 0 for finite o, turns NaN for any Inf / NaN
         double* const dbase = dst + fr.dst + cb + lane;
 #pragma unroll
         for (int l = 0; l < CT && ok; ++l) {  // lanes past u skip the z-pass and stores
@@ -206,7 +212,6 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
 #pragma unroll
               for (int i = 0; i < C0; ++i) {
                 dl[do1[j] + do0[i]] = o[i + C0 * j];
-                chk = fma(o[i + C0 * j], 0.0, chk);
               }
           } else {
 #pragma unroll
@@ -215,18 +220,13 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
               double* const dj = dl + do1[j];
 #pragma unroll
               for (int i = 0; i < C0; ++i)
-                if (ok0[i]) {
-                  dj[do0[i]] = o[i + C0 * j];
-                  chk = fma(o[i + C0 * j], 0.0, chk);
-                }
+                if (ok0[i]) dj[do0[i]] = o[i + C0 * j];
             }
           }
         }
-        raise_flag(flag, !isfinite(chk));
         continue;
       }
       // ---- z-pass of this block (lanes past u skip it and the synthesis) -----------
-      double chk = 0.0;  // fma(o, 0, chk) stays 0 for finite o, turns NaN for any Inf / NaN
       if (ok) {
         double M[NM];
         const int slot0 = w2 % L;
@@ -283,12 +283,11 @@ __global__ void __launch_bounds__(128, MINB) gram_slide_kernel(DevOp op, const d
 #pragma unroll
               for (int a = 0; a < D; ++a) o = fma(s0[i * 4 + a], R[a], o);
               dj[do0[i]] = o;
-              chk = fma(o, 0.0, chk);
             }
           }
         }
       }  // ok
-      raise_flag(flag, !isfinite(chk));
     }
   }
+  raise_flag(flag, !isfinite(chk));
 }
