@@ -273,7 +273,7 @@ __device__ __forceinline__ void tile_compute(const TileHdr& H, const DevOp& op, 
   double* const hdst = dst + H.dst_off;
 #pragma unroll 1
   for (int idx = threadIdx.x; idx < cnt; idx += NTH) {
-    const int blk = int(__umulhi(unsigned(idx), umag));
+    const int blk = u == 1 ? idx : int(__umulhi(unsigned(idx), umag));  // (no 32-bit reciprocal of 1)
     const int q = idx - blk * u;
     const int b2 = int((unsigned(blk) * n1mag) >> 16);
     const int b1 = blk - b2 * n1;

@@ -848,7 +848,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     // exact unknown split of the flattened item index (idx < 9 u) through a 32-bit reciprocal
     const bool exact = uint64_t(9) * u * uint64_t(u) < (uint64_t(1) << 32);
     if (smem <= 220 * 1024 && exact) {
-      const unsigned umag = unsigned((uint64_t(1) << 32) / unsigned(u) + 1);
+      const unsigned umag = u > 1 ? unsigned((uint64_t(1) << 32) / unsigned(u) + 1) : 0u;  // u = 1: unused
       const int64_t tiles = n_faces * int64_t(nt) * nt;
 #define TH_TILEK(TENSOR, NTH, MINB)                                                                         \
   do {                                                                                                      \

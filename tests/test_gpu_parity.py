@@ -194,6 +194,36 @@ def test_pool_interp_batch(th, scheme, p):
         assert rel(out[f], want) <= TOL, (f, rel(out[f], want))
 
 
+@pytest.mark.parametrize("u", (1, 33, 65, 130))
+@pytest.mark.parametrize("scheme,p", (("tensor_linear", 9), ("order2", 9), ("order3", 9), ("order2", 17)))
+def test_pool_interp_unknown_counts(th, scheme, p, u):
+    """Interpolation across unknown counts: the staged tile kernel's flattened (block, unknown)
+    items and its [unknown][cell] box at u = 1 (one item per block), 33 / 65 (items straddling
+    warps), 130 (a 156 KB box pair: one CTA per SM); the slide's ragged 32-unknown chunks."""
+    import torch
+
+    k = 3
+    rng = np.random.default_rng(u * 7 + p)
+    E = p + 2 * k
+    n_patch, n_face = 5, 12
+    pool = rng.standard_normal((n_patch, E ** 3 * u))
+    cid = rng.integers(0, n_patch, n_face)
+    nrm, sid, seg = np.arange(n_face) % 3, (np.arange(n_face) // 3) % 2, rng.integers(0, 9, n_face)
+    op = th.operators.DEFAULT_CACHE.device_operator("interpolate", scheme, p, k)
+    batch = th.FaceBatch(op, th.pool_interp_faces(p, k, u, cid, nrm, sid, seg), u)
+    dev = torch.device("cuda")
+    dst = torch.full((n_face * k * p * p * u,), np.nan, dtype=torch.float64, device=dev)
+    batch.launch(torch.from_numpy(pool.reshape(-1)).to(dev), dst)
+    out = dst.cpu().numpy().reshape(n_face, -1)
+    assert not batch.nonfinite()
+    for f in range(n_face):
+        lo, ext = _interp_box(p, k, int(nrm[f]), int(sid[f]))
+        box = _world_box(pool, E, u, int(cid[f]), lo, ext)
+        cfg = th.FaceConfig("xyz"[nrm[f]], ("negative", "positive")[sid[f]], int(seg[f]), p, k, u)
+        want = oracle_run(cfg, scheme, "interpolate", None, box)
+        assert rel(out[f], want) <= TOL, (scheme, p, u, f, rel(out[f], want))
+
+
 @pytest.mark.parametrize("scheme", ("tensor_linear", "matrix_linear", "order2", "order3"))
 @pytest.mark.parametrize("p,half", ((9, None), (17, None), (9, "inner"), (9, "outer")))
 def test_pool_restrict_batch(th, scheme, p, half):
@@ -336,7 +366,7 @@ def test_alternative_kernel_paths(th, env):
     here = os.path.dirname(os.path.abspath(__file__))
     res = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_parity.py"),
-         "-k", "exchange_all_faces_small or pool_interp_batch or pool_restrict_batch or transposed"],
+         "-k", "exchange_all_faces_small or pool_interp_batch or pool_restrict_batch or transposed or unknown_counts"],
         env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
 
