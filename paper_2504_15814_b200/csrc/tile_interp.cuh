@@ -149,8 +149,11 @@ __device__ __forceinline__ void tile_item(const double* w, const double* r0, con
   double T[3][NT];  // per window slice z: x / y projections
 #pragma unroll
   for (int z = 0; z < 3; ++z) {
+    double mm[3][3];  // Gram: x moments of the slice's three lines
+    if constexpr (TENSOR) {
 #pragma unroll
-    for (int t = 0; t < NT; ++t) T[z][t] = 0.0;
+      for (int t = 0; t < NT; ++t) T[z][t] = 0.0;
+    }
 #pragma unroll
     for (int y = 0; y < 3; ++y) {
       double v[3];
@@ -166,15 +169,10 @@ __device__ __forceinline__ void tile_item(const double* w, const double* r0, con
           for (int c1 = 0; c1 < 3; ++c1) T[z][c0 + 3 * c1] = fma(r1[c1 * 3 + y], tx, T[z][c0 + 3 * c1]);
         }
       } else {
-        double m[3];
-        gram_moments<3, 3>(v, m);
-        int t = 0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b + a < 3; ++b, ++t) gacc(T[z][t], Gram<3>::P(b, y), m[a]);
+        gram_moments<3, 3>(v, mm[y]);
       }
     }
+    if constexpr (!TENSOR) gram_y<3, 3>(mm, T[z]);  // y moments of the x moments (symmetric sums)
     // finiteness of the inputs: every value of the slice enters T[z][0] (Gram: the plain sum;
     // tensor: an fma chain through all of them), so a NaN / Inf anywhere turns chk NaN
     chk = fma(T[z][0], 0.0, chk);
