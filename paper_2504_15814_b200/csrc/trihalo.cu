@@ -771,6 +771,35 @@ int32_t th_operator_export_rows(const th_operator* op, int32_t selector, int64_t
   return TH_OK;
 }
 
+// Resident CTAs per SM of a kernel at a dynamic shared-memory size (raising the kernel's
+// dynamic-smem limit first), computed once per (device, kernel, size): launches stay cheap and
+// concurrent callers share the cache.
+static cudaError_t resident_ctas(const void* kfn, int nth, size_t smem, int* per_sm) {
+  struct Entry {
+    int dev;
+    const void* fn;
+    size_t smem;
+    int per_sm;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& c : cache)
+    if (c.dev == dev && c.fn == kfn && c.smem == smem) {
+      *per_sm = c.per_sm;
+      return cudaSuccess;
+    }
+  if (smem > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) != cudaSuccess)
+    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nth, smem)) != cudaSuccess) return e;
+  cache.push_back({dev, kfn, smem, *per_sm});
+  return cudaSuccess;
+}
+
 int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, const th_face* faces, int64_t n_faces,
                        int32_t u, int32_t* flag, void* stream) {
   if (!op) return fail(TH_ERR_CONFIG, "NULL operator");
@@ -853,9 +882,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
 #define TH_TILEK(TENSOR, NTH, MINB)                                                                         \
   do {                                                                                                      \
     auto kfn = tile_interp_kernel<TENSOR, NTH, MINB>;                                                       \
-    if (smem > 48 * 1024) TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
     int per_sm = 0;                                                                                         \
-    TH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NTH, smem));                       \
+    TH_CUDA(resident_ctas(reinterpret_cast<const void*>(kfn), NTH, smem, &per_sm));                        \
     const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));          \
     kfn<<<tblocks, NTH, smem, s>>>(op->dev, src, dst, faces, tiles, nt, pitch, u, umag, flag);              \
   } while (0)
