@@ -194,12 +194,13 @@ def test_pool_interp_batch(th, scheme, p):
         assert rel(out[f], want) <= TOL, (f, rel(out[f], want))
 
 
-@pytest.mark.parametrize("u", (1, 33, 65, 130))
+@pytest.mark.parametrize("u", (1, 33, 65, 130, 200))
 @pytest.mark.parametrize("scheme,p", (("tensor_linear", 9), ("order2", 9), ("order3", 9), ("order2", 17)))
 def test_pool_interp_unknown_counts(th, scheme, p, u):
     """Interpolation across unknown counts: the staged tile kernel's flattened (block, unknown)
     items and its [unknown][cell] box at u = 1 (one item per block), 33 / 65 (items straddling
-    warps), 130 (a 156 KB box pair: one CTA per SM); the slide's ragged 32-unknown chunks."""
+    warps), 130 (a 156 KB box pair: one CTA per SM), 200 (boxes beyond shared memory: the
+    per-warp slide takes over); the slide's ragged 32-unknown chunks."""
     import torch
 
     k = 3
