@@ -1,0 +1,316 @@
+// Staged tile interpolation for order3 (5-cell Gram windows), included by
+// trihalo.cu after tile_interp.cuh.
+//
+// Same arithmetic as gram_slide_kernel<3, 0> (the reference's least-squares rows,
+// taylor.py:171-219, as the projection onto total degree <= 3 with the window's
+// discrete Gram polynomials), organised so that no source load sits on a thread's
+// critical path and the normal / t1 passes are shared by every block that needs them:
+//
+//  * a CTA owns a tile = (face, chunk of <= 31 unknowns); the face's source support
+//    (5 normal x <= 7 x <= 7 coarse cells: the whole segment at p <= 9) is copied into
+//    a shared-memory box with 8-byte cp.async;
+//  * phase A, items (t2 slice z, unknown): the x (normal) Gram moments of the slice's
+//    <= 7 lines, then the y moments of each distinct t1 window start s (<= 3), written
+//    as T[s][z][pair] to a second shared region.  The box is then free: the NEXT
+//    tile's copy is issued before phase B, so it lands while phase B computes;
+//  * phase B, items (block, unknown) with the unknown fastest: the block's z moments
+//    from its 5 T slices, the synthesis at its <= 27 children, direct stores (a warp
+//    writes contiguous runs of unknowns).
+// Two CTAs per SM (2 x 114 KB of shared memory) alternate between the phases.
+#pragma once
+
+constexpr int T3Y = 7;                    // box extent along t1 / t2 (three 5-cell windows within 7 cells)
+constexpr int T3BOX = 5 * T3Y * T3Y;      // 245 cells: odd pitch, conflict-free 8-byte accesses
+constexpr int T3TP = 3 * T3Y * 10 + 1;    // T region per unknown: [start s][z][pair t], odd pitch
+constexpr int T3CMAX = 31;                // unknowns per tile (2 CTAs per SM fit in shared memory)
+
+struct Tile3Hdr {
+  int64_t src_off;     // source cell (normal window start, box origin along t1 / t2)
+  int64_t dst_off;     // target origin of the face
+  int64_t sn, s1, s2;  // signed source strides (reference frame)
+  int64_t dn, d1, d2;  // target strides
+  int lo1, lo2;        // target index origin of the segment along t1 / t2
+  int g0, g1, n1, g2, n2;
+  int y0, ny, z0, nz;  // the box along t1 / t2
+  int cb, cn;          // the tile's unknowns [cb, cb + cn)
+  unsigned n1mag, cnmag;
+  int narrow;          // every target offset inside the face fits 32 bits
+};
+
+// first unknown of chunk c of nch; align: boundaries rounded down to 4 unknowns (32-byte
+// sectors of the AoS cells), chosen by the host when every chunk still fits T3CMAX
+__device__ __forceinline__ int tile3_bound(int c, int nch, int u, int align) {
+  if (c >= nch) return u;
+  const int b = c * u / nch;
+  return align ? (b & ~3) : b;
+}
+
+__device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __restrict__ faces, int64_t tile,
+                                             int nch, int align, int u, Tile3Hdr& H) {
+  const int64_t f = tile / nch;
+  const int c = int(tile - f * nch);
+  FaceRef fr;
+  decode_face(faces + f, op, fr);
+  H.g0 = fr.g0;
+  H.g1 = fr.g1;
+  H.n1 = fr.n1;
+  H.g2 = fr.g2;
+  H.n2 = fr.n2;
+  H.dst_off = fr.dst;
+  H.sn = fr.sn;
+  H.s1 = fr.s1;
+  H.s2 = fr.s2;
+  H.dn = fr.dn;
+  H.d1 = fr.d1;
+  H.d2 = fr.d2;
+  H.lo1 = fr.lo1;
+  H.lo2 = fr.lo2;
+  H.cb = tile3_bound(c, nch, u, align);
+  H.cn = tile3_bound(c + 1, nch, u, align) - H.cb;
+  if (H.n1 <= 0 || H.n2 <= 0) {
+    H.n1 = H.n2 = 1;
+    H.y0 = H.z0 = 0;
+    H.ny = H.nz = 0;
+    H.cn = 0;
+  } else {
+    H.y0 = __ldg(&op.grp1[H.g1]).x;
+    H.ny = __ldg(&op.grp1[H.g1 + H.n1 - 1]).x + 5 - H.y0;
+    H.z0 = __ldg(&op.grp1[H.g2]).x;
+    H.nz = __ldg(&op.grp1[H.g2 + H.n2 - 1]).x + 5 - H.z0;
+  }
+  const int4 G0 = __ldg(&op.grp0[fr.g0]);
+  H.src_off = fr.src0 + int64_t(G0.x) * fr.sn + int64_t(H.y0) * fr.s1 + int64_t(H.z0) * fr.s2 + H.cb;
+  H.n1mag = recip16(H.n1);
+  H.cnmag = recip16(max(H.cn, 1));
+  const int64_t lim = int64_t(1) << 21;
+  auto small = [lim](int64_t s) { return s > -lim && s < lim; };
+  H.narrow = small(fr.dn) && small(fr.d1) && small(fr.d2) && op.p <= 64 && u <= (1 << 20);
+}
+
+// cp.async copies of the tile's box into box[q][x + 5 (y + T3Y z)] (warps over lines (y, z),
+// lanes over the chunk's unknowns)
+template <int NTH>
+__device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __restrict__ src, double* box) {
+  constexpr int NW = NTH / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane >= H.cn) return;
+  const int ny = H.ny, nz = H.nz;
+  const int64_t sn = H.sn, s1 = H.s1, s2 = H.s2;
+  const double* const base = src + H.src_off + lane;
+  double* const bq = box + lane * T3BOX;
+  for (int r = warp; r < ny * nz; r += NW) {
+    const int z = r / ny, y = r - z * ny;
+    const double* row = base + (int64_t(y) * s1 + int64_t(z) * s2);
+    double* const drow = bq + 5 * (y + T3Y * z);
+#pragma unroll
+    for (int x = 0; x < 5; ++x) cp_async8(drow + x, row + int64_t(x) * sn);
+  }
+}
+
+// L2 prefetch of a tile's box: the <= 3 128-byte lines of each cell's chunk
+template <int NTH>
+__device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const double* __restrict__ src) {
+  const int n = H.ny * H.nz * 5;
+  const int last = H.cn * 8 - 1;
+  const char* const base = reinterpret_cast<const char*>(src + H.src_off);
+  for (int c = threadIdx.x; c < n; c += NTH) {
+    const int x = c % 5, r = c / 5, z = r / H.ny, y = r - z * H.ny;
+    const char* const pc = base + 8 * (int64_t(x) * H.sn + int64_t(y) * H.s1 + int64_t(z) * H.s2);
+    l2_prefetch_line(pc);
+    l2_prefetch_line(pc + 128);
+    l2_prefetch_line(pc + last);
+  }
+}
+
+// phase A: item (z, q) -> T[q][s][z][t] for every window start s of the box (NY = box
+// extent along t1, compile-time so the line moments stay in registers)
+template <int NTH, int NY>
+__device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double* box, double* tr, double& chk) {
+  const int z = threadIdx.x >> 5, q = threadIdx.x & 31;
+  {
+    const double* bz = box + q * T3BOX + 5 * T3Y * z;
+    double mm[NY][4];
+#pragma unroll
+    for (int y = 0; y < NY; ++y) {
+      double v[5];
+#pragma unroll
+      for (int x = 0; x < 5; ++x) v[x] = bz[5 * y + x];
+      gram_moments<5, 4>(v, mm[y]);
+      asm volatile("" ::: "memory");  // one line of loads live at a time (register budget)
+    }
+    double* const tq = tr + q * T3TP + 10 * z;
+#pragma unroll
+    for (int s = 0; s + 4 < NY; ++s) {
+      double w[5][4];
+#pragma unroll
+      for (int y = 0; y < 5; ++y)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) w[y][a] = mm[s + y][a];
+      double T[10];
+      gram_y<5, 4>(w, T);
+      // every box value enters some window's T_00 (the windows cover the box's t1 extent)
+      chk = fma(T[0], 0.0, chk);
+#pragma unroll
+      for (int t = 0; t < 10; ++t) tq[s * (10 * T3Y) + t] = T[t];
+    }
+  }
+}
+
+template <int NTH>
+__device__ __forceinline__ void tile3_phase_a(const Tile3Hdr& H, const double* box, double* tr, double& chk) {
+  // item (z, q) = (warp, lane): conflict-free box / T accesses (odd pitches)
+  if ((threadIdx.x >> 5) >= H.nz || (threadIdx.x & 31) >= H.cn) return;
+  if (H.ny == 5) tile3_phase_a_ny<NTH, 5>(H, box, tr, chk);
+  else if (H.ny == 6) tile3_phase_a_ny<NTH, 6>(H, box, tr, chk);
+  else if (H.ny == 7) tile3_phase_a_ny<NTH, 7>(H, box, tr, chk);
+}
+
+// phase B: item (block, q): z moments from T, synthesis at the children, stores
+template <int NTH, bool ALL, typename OFF>
+__device__ __forceinline__ void tile3_item(const double* tq, const double* r0, const double* r1, const double* r2,
+                                           double* __restrict__ hdst, OFF qo, OFF d1, OFF d2, const OFF (&do0)[3],
+                                           const bool (&ok0)[3], const bool (&ok1)[3], const bool (&ok2)[3]) {
+  double M[20];
+  {
+    int t = 0, mi = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b + a < 4; ++b, ++t) {
+        double col[5];
+#pragma unroll
+        for (int z = 0; z < 5; ++z) col[z] = tq[10 * z + t];
+        gram_moments_n<5>(col, M + mi, 4 - a - b);
+        mi += 4 - a - b;
+        asm volatile("" ::: "memory");  // one column of loads live at a time
+      }
+  }
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    if (!ALL && !ok2[l]) continue;
+    asm volatile("" ::: "memory");  // table values re-read per child (not hoisted into registers)
+    double Q[10];
+    int t = 0, mi = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b + a < 4; ++b, ++t) {
+        Q[t] = 0.0;
+#pragma unroll
+        for (int c = 0; c + b + a < 4; ++c, ++mi) Q[t] = fma(r2[l * 4 + c], M[mi], Q[t]);
+      }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (!ALL && !ok1[j]) continue;
+      double R[4];
+      int tt = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        R[a] = 0.0;
+#pragma unroll
+        for (int b = 0; b + a < 4; ++b, ++tt) R[a] = fma(r1[j * 4 + b], Q[tt], R[a]);
+      }
+      const OFF oj = qo + OFF(l) * d2 + OFF(j) * d1;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double oi = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) oi = fma(r0[i * 4 + a], R[a], oi);
+        if (ALL || ok0[i]) *elem(hdst, oj + do0[i]) = oi;
+      }
+    }
+  }
+}
+
+template <int NTH, typename OFF>
+__device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op, double* __restrict__ dst,
+                                              const double* tr, const double* stab, const double* stab0,
+                                              const int4* sgrp) {
+  const int4 G0 = __ldg(&op.grp0[H.g0]);
+  bool ok0[3];
+  OFF do0[3];
+  bool all0 = true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int t = G0.z + i;
+    ok0[i] = i < G0.w && t >= 0 && t < op.k;
+    do0[i] = OFF(t) * OFF(H.dn);
+    all0 &= ok0[i];
+  }
+  const OFF d1 = OFF(H.d1), d2 = OFF(H.d2);
+  const int p = op.p, lo1 = H.lo1, lo2 = H.lo2, n1 = H.n1, g1b = H.g1, g2b = H.g2, y0 = H.y0, z0 = H.z0;
+  const int cb = H.cb;
+  const int g0tw = H.g0 * 12;
+  double* const hdst = dst + H.dst_off;
+  // item (block, q) = (warp, lane): table reads are broadcasts, T reads conflict-free
+  const int blk = threadIdx.x >> 5, q = threadIdx.x & 31;
+  if (blk < n1 * H.n2 && q < H.cn) {
+    const int b2 = int((unsigned(blk) * H.n1mag) >> 16);
+    const int b1 = blk - b2 * n1;
+    const int g1 = g1b + b1, g2 = g2b + b2;
+    const int4 G1 = sgrp[g1], G2 = sgrp[g2];
+    bool ok1[3], ok2[3];
+    bool all = all0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      ok1[j] = j < G1.w && unsigned(G1.z + j - lo1) < unsigned(p);
+      ok2[j] = j < G2.w && unsigned(G2.z + j - lo2) < unsigned(p);
+      all &= ok1[j] & ok2[j];
+    }
+    const double* tq = tr + (q * T3TP + (G1.x - y0) * (10 * T3Y) + 10 * (G2.x - z0));
+    const OFF qo = OFF(G1.z - lo1) * d1 + OFF(G2.z - lo2) * d2 + OFF(cb + q);
+    const double* r1 = stab + g1 * 12;
+    const double* r2 = stab + g2 * 12;
+    const double* r0 = stab0 + opaque(g0tw);
+    if (all) tile3_item<NTH, true, OFF>(tq, r0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+    else tile3_item<NTH, false, OFF>(tq, r0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+  }
+}
+
+// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | stab0 [G0][12] | box[cmax][T3BOX] | T[cmax][T3TP]
+template <int NTH, int MINB>
+__global__ void __launch_bounds__(NTH, MINB)
+    tile3_interp_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
+                        const th_face* __restrict__ faces, int64_t n_tiles, int nch, int align, int cmax, int u,
+                        int32_t* flag) {
+  static_assert(NTH == 32 * 9, "one warp per block of the 3 x 3 tile (phase B) and per t2 slice (phase A)");
+  extern __shared__ __align__(16) double smem_t3[];
+  __shared__ Tile3Hdr Hs[4];  // tiles it (computing), it + 1 (fetching), it + 2 (L2 prefetch), it + 3 (decoding)
+  const int G1n = op.G1;
+  int4* const sgrp = reinterpret_cast<int4*>(smem_t3);
+  double* const stab = smem_t3 + 2 * G1n;
+  double* const stab0 = stab + ((G1n * 12 + 1) & ~1);
+  double* const box = smem_t3 + tile_box_offset(12, op.G0, G1n);
+  double* const tr = box + cmax * T3BOX;
+  for (int i = threadIdx.x; i < G1n; i += NTH) sgrp[i] = __ldg(&op.grp1[i]);
+  for (int i = threadIdx.x; i < G1n * 12; i += NTH) stab[i] = __ldg(op.synth1 + i);
+  for (int i = threadIdx.x; i < op.G0 * 12; i += NTH) stab0[i] = __ldg(op.synth0 + i);
+  constexpr int DEC = NTH - 1;
+  const int64_t t0 = blockIdx.x, step = gridDim.x;
+  if (threadIdx.x == DEC)
+    for (int i = 0; i < 3; ++i)
+      if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nch, align, u, Hs[i]);
+  __syncthreads();
+  if (t0 < n_tiles) tile3_fetch<NTH>(Hs[0], src, box);
+  cp_async_commit();
+  if (t0 + step < n_tiles) tile3_prefetch_l2<NTH>(Hs[1], src);
+  double chk = 0.0;  // fma(T00, 0, chk) stays 0 for finite inputs, turns NaN for any Inf / NaN
+  int it = 0;
+  for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
+    cp_async_wait_all();
+    __syncthreads();  // this tile's box landed; the previous tile's phase B is done with T
+    const Tile3Hdr& H = Hs[it & 3];
+    tile3_phase_a<NTH>(H, box, tr, chk);
+    __syncthreads();  // T complete, the box is free
+    if (tile + step < n_tiles) tile3_fetch<NTH>(Hs[(it + 1) & 3], src, box);
+    cp_async_commit();
+    // the tile after next into L2, so that its copies above find it there one iteration later
+    if (tile + 2 * step < n_tiles) tile3_prefetch_l2<NTH>(Hs[(it + 2) & 3], src);
+    if (threadIdx.x == DEC && tile + 3 * step < n_tiles)
+      tile3_decode(op, faces, tile + 3 * step, nch, align, u, Hs[(it + 3) & 3]);
+    if (H.narrow) tile3_phase_b<NTH, int>(H, op, dst, tr, stab, stab0, sgrp);
+    else tile3_phase_b<NTH, int64_t>(H, op, dst, tr, stab, stab0, sgrp);
+  }
+  cp_async_wait_all();
+  raise_flag(flag, !isfinite(chk));
+}

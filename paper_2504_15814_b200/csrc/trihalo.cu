@@ -18,6 +18,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/trihalo_b200.h"
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "gram_slide.cuh"
 #include "stage_slide.cuh"
 #include "tile_interp.cuh"
+#include "tile_interp3.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -388,6 +390,8 @@ struct th_operator {
   // staged tile interpolation (tile_interp.cuh): mode (0 = not eligible, 1 = tensor_linear,
   // 2 = order2 Gram) and tiles per face axis
   int ti_mode = 0, ti_nt = 0;
+  // staged order3 tile interpolation (tile_interp3.cuh) eligibility
+  bool t3_ok = false;
 };
 
 namespace {
@@ -538,6 +542,31 @@ void prepare_tile(th_operator* op) {
   if (nt > 1 && !multi) return;
   op->ti_mode = mode;
   op->ti_nt = nt;
+}
+
+// Staged order3 tile interpolation eligibility (tile_interp3.cuh): one normal group with a
+// 5-cell window and <= 3 children; tangential groups with 5-cell windows, <= 3 children and
+// non-decreasing starts; every segment axis holds <= 3 groups whose windows span <= T3Y
+// cells (one tile per face: p <= 9).
+void prepare_tile3(th_operator* op) {
+  const th::HostOperator& h = op->host;
+  op->t3_ok = false;
+  if (h.role != 0 || h.scheme != TH_SCHEME_ORDER3 || !h.gram_ok || h.fast_C0 != 3 || h.synth[0].empty() ||
+      h.synth[1].empty() || h.groups[0].size() != 1 || h.groups[1].empty())
+    return;
+  const th::Group& g0 = h.groups[0][0];
+  if (g0.winL != 5 || g0.tgtN < 1 || g0.tgtN > 3) return;
+  const auto& g1 = h.groups[1];
+  for (size_t j = 0; j < g1.size(); ++j) {
+    if (g1[j].winL != 5 || g1[j].tgtN < 1 || g1[j].tgtN > 3) return;
+    if (j > 0 && g1[j].win0 < g1[j - 1].win0) return;
+  }
+  for (int c = 0; c < 3; ++c) {
+    const int a = h.seg_g[c][0], n = h.seg_g[c][1] - a;
+    if (n > 3) return;
+    if (n > 0 && g1[a + n - 1].win0 + 5 - g1[a].win0 > T3Y) return;
+  }
+  op->t3_ok = true;
 }
 
 // launch geometry of the slice-staged kernels (stage_slide.cuh) for u unknowns;
@@ -707,6 +736,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   prepare_restrict(op);
   prepare_stage(op);
   prepare_tile(op);
+  prepare_tile3(op);
   if (!upload_to_device) {
     *out = op;
     return TH_OK;
@@ -771,9 +801,11 @@ int32_t th_operator_export_rows(const th_operator* op, int32_t selector, int64_t
   return TH_OK;
 }
 
-// Resident CTAs per SM of a kernel at a dynamic shared-memory size (raising the kernel's
-// dynamic-smem limit first), computed once per (device, kernel, size): launches stay cheap and
-// concurrent callers share the cache.
+// Resident CTAs per SM of a kernel at a dynamic shared-memory size, computed once per
+// (device, kernel, size): launches stay cheap and concurrent callers share the cache.  The
+// kernel's dynamic-smem limit is raised to the device's opt-in maximum the first time the
+// kernel is seen on a device (a limit raised only to the first size seen would reject a later,
+// larger launch of the same kernel).
 static cudaError_t resident_ctas(const void* kfn, int nth, size_t smem, int* per_sm) {
   struct Entry {
     int dev;
@@ -783,6 +815,7 @@ static cudaError_t resident_ctas(const void* kfn, int nth, size_t smem, int* per
   };
   static std::mutex mu;
   static std::vector<Entry> cache;
+  static std::vector<std::pair<int, const void*>> raised;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -792,9 +825,16 @@ static cudaError_t resident_ctas(const void* kfn, int nth, size_t smem, int* per
       *per_sm = c.per_sm;
       return cudaSuccess;
     }
-  if (smem > 48 * 1024 &&
-      (e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) != cudaSuccess)
-    return e;
+  if (std::find(raised.begin(), raised.end(), std::make_pair(dev, kfn)) == raised.end()) {
+    int optin = 0;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, kfn)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - int(fa.sharedSizeBytes))) != cudaSuccess)
+      return e;
+    raised.emplace_back(dev, kfn);
+  }
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kfn, nth, smem)) != cudaSuccess) return e;
   cache.push_back({dev, kfn, smem, *per_sm});
   return cudaSuccess;
@@ -899,6 +939,35 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
         else TH_TILEK(false, 192, 2);
       }
 #undef TH_TILEK
+      TH_CUDA(cudaGetLastError());
+      return TH_OK;
+    }
+  }
+  //   TH_TILE3=0                 order3 interpolation through the per-warp slide instead of the
+  //                              staged two-phase tiles (tile_interp3.cuh)
+  static const int use_tile3 = [] { const char* e = std::getenv("TH_TILE3"); return e ? std::atoi(e) : 1; }();
+  if (use_tile3 && interp && op->t3_ok && !stage_interp) {
+    // tiles = (face, chunk of <= T3CMAX unknowns); chunk boundaries on 4-unknown (32-byte)
+    // sector edges when every chunk still fits
+    const int nch = (u + T3CMAX - 1) / T3CMAX;
+    int align = 1, cmax = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int b0 = (c * u / nch) & ~3, b1 = c + 1 < nch ? ((c + 1) * u / nch) & ~3 : u;
+      if (b1 - b0 > T3CMAX || b1 <= b0) align = 0;
+    }
+    for (int c = 0; c < nch; ++c) {
+      int b0 = c * u / nch, b1 = (c + 1) * u / nch;
+      if (align) b0 &= ~3, b1 = c + 1 < nch ? b1 & ~3 : u;
+      cmax = std::max(cmax, b1 - b0);
+    }
+    const size_t smem = 8 * (size_t(tile_box_offset(12, op->dev.G0, op->dev.G1)) + size_t(cmax) * (T3BOX + T3TP));
+    const int64_t tiles = n_faces * int64_t(nch);
+    if (smem <= 227 * 1024) {
+      auto kfn = tile3_interp_kernel<288, 2>;
+      int per_sm = 0;
+      TH_CUDA(resident_ctas(reinterpret_cast<const void*>(kfn), 288, smem, &per_sm));
+      const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));
+      kfn<<<tblocks, 288, smem, s>>>(op->dev, src, dst, faces, tiles, nch, align, cmax, u, flag);
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
