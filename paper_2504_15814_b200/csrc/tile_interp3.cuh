@@ -21,8 +21,16 @@
 
 constexpr int T3Y = 7;                    // box extent along t1 / t2 (three 5-cell windows within 7 cells)
 constexpr int T3BOX = 5 * T3Y * T3Y;      // 245 cells: odd pitch, conflict-free 8-byte accesses
-constexpr int T3TP = 3 * T3Y * 10 + 1;    // T region per unknown: [start s][z][pair t], odd pitch
+constexpr int T3TP = 3 * T3Y * 10;        // T region per unknown: [start s][z][pair t]; 210 = 2 mod 16
+                                          // doubles: 16-byte accesses of consecutive unknowns are
+                                          // conflict-free (pairs of T values per LDS.128 / STS.128)
 constexpr int T3CMAX = 31;                // unknowns per tile (2 CTAs per SM fit in shared memory)
+
+// the normal synthesis table of the operator's single normal group, [child][4], passed as a
+// kernel parameter: the synthesis FMAs take it straight from the constant bank
+struct T3Syn0 {
+  double v[12];
+};
 
 struct Tile3Hdr {
   int64_t src_off;     // source cell (normal window start, box origin along t1 / t2)
@@ -36,6 +44,12 @@ struct Tile3Hdr {
   unsigned n1mag, cnmag;
   int narrow;          // every target offset inside the face fits 32 bits
 };
+
+// 4 table doubles through two 16-byte shared-memory loads (p 16-byte aligned)
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+}
 
 // first unknown of chunk c of nch; align: boundaries rounded down to 4 unknowns (32-byte
 // sectors of the AoS cells), chosen by the host when every chunk still fits T3CMAX
@@ -87,34 +101,41 @@ __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __r
   H.narrow = small(fr.dn) && small(fr.d1) && small(fr.d2) && op.p <= 64 && u <= (1 << 20);
 }
 
-// cp.async copies of the tile's box into box[q][x + 5 (y + T3Y z)] (warps over lines (y, z),
-// lanes over the chunk's unknowns)
+// cp.async copies of the tile's box into box[q][x + 5 (y + T3Y z)]: warps over the box's source
+// lines (y, z) (all 9 warps, so the copies are issued quickly), lanes over the chunk's unknowns
 template <int NTH>
 __device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __restrict__ src, double* box) {
   constexpr int NW = NTH / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane >= H.cn) return;
-  const int ny = H.ny, nz = H.nz;
+  const int ny = H.ny, nl = H.ny * H.nz;
+  const unsigned nymag = recip16(max(ny, 1));
   const int64_t sn = H.sn, s1 = H.s1, s2 = H.s2;
-  const double* const base = src + H.src_off + lane;
+  const double* const base = src + (H.src_off + lane);
   double* const bq = box + lane * T3BOX;
-  for (int r = warp; r < ny * nz; r += NW) {
-    const int z = r / ny, y = r - z * ny;
-    const double* row = base + (int64_t(y) * s1 + int64_t(z) * s2);
+#pragma unroll 1
+  for (int r = warp; r < nl; r += NW) {
+    const int z = int((unsigned(r) * nymag) >> 16), y = r - z * ny;
+    const double* cell = base + (int64_t(y) * s1 + int64_t(z) * s2);
     double* const drow = bq + 5 * (y + T3Y * z);
 #pragma unroll
-    for (int x = 0; x < 5; ++x) cp_async8(drow + x, row + int64_t(x) * sn);
+    for (int x = 0; x < 5; ++x, cell += sn) cp_async8(drow + x, cell);
   }
 }
 
-// L2 prefetch of a tile's box: the <= 3 128-byte lines of each cell's chunk
+// L2 prefetch of a tile's box: one source cell per thread, the <= 3 128-byte lines of its chunk
 template <int NTH>
 __device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const double* __restrict__ src) {
   const int n = H.ny * H.nz * 5;
-  const int last = H.cn * 8 - 1;
+  if (H.cn <= 0) return;
+  const int last = H.cn * 8 - 1, ny = H.ny;
+  const unsigned nymag = recip16(max(ny, 1));
   const char* const base = reinterpret_cast<const char*>(src + H.src_off);
+#pragma unroll 1
   for (int c = threadIdx.x; c < n; c += NTH) {
-    const int x = c % 5, r = c / 5, z = r / H.ny, y = r - z * H.ny;
+    const int r = int((unsigned(c) * 13108u) >> 16);  // c / 5 (exact for c < 16384)
+    const int x = c - 5 * r;
+    const int z = int((unsigned(r) * nymag) >> 16), y = r - z * ny;
     const char* const pc = base + 8 * (int64_t(x) * H.sn + int64_t(y) * H.s1 + int64_t(z) * H.s2);
     l2_prefetch_line(pc);
     l2_prefetch_line(pc + 128);
@@ -151,7 +172,8 @@ __device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double
       // every box value enters some window's T_00 (the windows cover the box's t1 extent)
       chk = fma(T[0], 0.0, chk);
 #pragma unroll
-      for (int t = 0; t < 10; ++t) tq[s * (10 * T3Y) + t] = T[t];
+      for (int t = 0; t < 10; t += 2)
+        *reinterpret_cast<double2*>(tq + s * (10 * T3Y) + t) = make_double2(T[t], T[t + 1]);
     }
   }
 }
@@ -167,28 +189,33 @@ __device__ __forceinline__ void tile3_phase_a(const Tile3Hdr& H, const double* b
 
 // phase B: item (block, q): z moments from T, synthesis at the children, stores
 template <int NTH, bool ALL, typename OFF>
-__device__ __forceinline__ void tile3_item(const double* tq, const double* r0, const double* r1, const double* r2,
+__device__ __forceinline__ void tile3_item(const double* tq, const T3Syn0& s0, const double* r1, const double* r2,
                                            double* __restrict__ hdst, OFF qo, OFF d1, OFF d2, const OFF (&do0)[3],
                                            const bool (&ok0)[3], const bool (&ok1)[3], const bool (&ok2)[3]) {
+  // z moments of the 10 (a, b) columns, two columns per 16-byte load; M index of column
+  // t = (a, b) is MO[t] (a-major, 4 - a - b moments each)
+  constexpr int MO[10] = {0, 4, 7, 9, 10, 13, 15, 16, 18, 19};
+  constexpr int MN[10] = {4, 3, 2, 1, 3, 2, 1, 2, 1, 1};
   double M[20];
-  {
-    int t = 0, mi = 0;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+  for (int t = 0; t < 10; t += 2) {
+    double ca[5], cb[5];
 #pragma unroll
-      for (int b = 0; b + a < 4; ++b, ++t) {
-        double col[5];
-#pragma unroll
-        for (int z = 0; z < 5; ++z) col[z] = tq[10 * z + t];
-        gram_moments_n<5>(col, M + mi, 4 - a - b);
-        mi += 4 - a - b;
-        asm volatile("" ::: "memory");  // one column of loads live at a time
-      }
+    for (int z = 0; z < 5; ++z) {
+      const double2 v = *reinterpret_cast<const double2*>(tq + 10 * z + t);
+      ca[z] = v.x;
+      cb[z] = v.y;
+    }
+    gram_moments_n<5>(ca, M + MO[t], MN[t]);
+    gram_moments_n<5>(cb, M + MO[t + 1], MN[t + 1]);
+    asm volatile("" ::: "memory");  // one column pair of loads live at a time
   }
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     if (!ALL && !ok2[l]) continue;
     asm volatile("" ::: "memory");  // table values re-read per child (not hoisted into registers)
+    double S2[4];
+    ld4(r2 + l * 4, S2);
     double Q[10];
     int t = 0, mi = 0;
 #pragma unroll
@@ -197,25 +224,28 @@ __device__ __forceinline__ void tile3_item(const double* tq, const double* r0, c
       for (int b = 0; b + a < 4; ++b, ++t) {
         Q[t] = 0.0;
 #pragma unroll
-        for (int c = 0; c + b + a < 4; ++c, ++mi) Q[t] = fma(r2[l * 4 + c], M[mi], Q[t]);
+        for (int c = 0; c + b + a < 4; ++c, ++mi) Q[t] = fma(S2[c], M[mi], Q[t]);
       }
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       if (!ALL && !ok1[j]) continue;
+      asm volatile("" ::: "memory");  // S1 re-read per child
+      double S1[4];
+      ld4(r1 + j * 4, S1);
       double R[4];
       int tt = 0;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         R[a] = 0.0;
 #pragma unroll
-        for (int b = 0; b + a < 4; ++b, ++tt) R[a] = fma(r1[j * 4 + b], Q[tt], R[a]);
+        for (int b = 0; b + a < 4; ++b, ++tt) R[a] = fma(S1[b], Q[tt], R[a]);
       }
       const OFF oj = qo + OFF(l) * d2 + OFF(j) * d1;
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         double oi = 0.0;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) oi = fma(r0[i * 4 + a], R[a], oi);
+        for (int a = 0; a < 4; ++a) oi = fma(s0.v[i * 4 + a], R[a], oi);  // constant-bank operands
         if (ALL || ok0[i]) *elem(hdst, oj + do0[i]) = oi;
       }
     }
@@ -224,7 +254,7 @@ __device__ __forceinline__ void tile3_item(const double* tq, const double* r0, c
 
 template <int NTH, typename OFF>
 __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op, double* __restrict__ dst,
-                                              const double* tr, const double* stab, const double* stab0,
+                                              const double* tr, const double* stab, const T3Syn0& s0,
                                               const int4* sgrp) {
   const int4 G0 = __ldg(&op.grp0[H.g0]);
   bool ok0[3];
@@ -240,7 +270,6 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
   const OFF d1 = OFF(H.d1), d2 = OFF(H.d2);
   const int p = op.p, lo1 = H.lo1, lo2 = H.lo2, n1 = H.n1, g1b = H.g1, g2b = H.g2, y0 = H.y0, z0 = H.z0;
   const int cb = H.cb;
-  const int g0tw = H.g0 * 12;
   double* const hdst = dst + H.dst_off;
   // item (block, q) = (warp, lane): table reads are broadcasts, T reads conflict-free
   const int blk = threadIdx.x >> 5, q = threadIdx.x & 31;
@@ -261,16 +290,16 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
     const OFF qo = OFF(G1.z - lo1) * d1 + OFF(G2.z - lo2) * d2 + OFF(cb + q);
     const double* r1 = stab + g1 * 12;
     const double* r2 = stab + g2 * 12;
-    const double* r0 = stab0 + opaque(g0tw);
-    if (all) tile3_item<NTH, true, OFF>(tq, r0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
-    else tile3_item<NTH, false, OFF>(tq, r0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+    if (all) tile3_item<NTH, true, OFF>(tq, s0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+    else tile3_item<NTH, false, OFF>(tq, s0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
   }
 }
 
-// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | stab0 [G0][12] | box[cmax][T3BOX] | T[cmax][T3TP]
+// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (unused [G0][12]) | box[cmax][T3BOX] (+1 to an
+// even count) | T[cmax][T3TP]
 template <int NTH, int MINB>
 __global__ void __launch_bounds__(NTH, MINB)
-    tile3_interp_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
+    tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
                         const th_face* __restrict__ faces, int64_t n_tiles, int nch, int align, int cmax, int u,
                         int32_t* flag) {
   static_assert(NTH == 32 * 9, "one warp per block of the 3 x 3 tile (phase B) and per t2 slice (phase A)");
@@ -279,12 +308,10 @@ __global__ void __launch_bounds__(NTH, MINB)
   const int G1n = op.G1;
   int4* const sgrp = reinterpret_cast<int4*>(smem_t3);
   double* const stab = smem_t3 + 2 * G1n;
-  double* const stab0 = stab + ((G1n * 12 + 1) & ~1);
   double* const box = smem_t3 + tile_box_offset(12, op.G0, G1n);
-  double* const tr = box + cmax * T3BOX;
+  double* const tr = box + ((cmax * T3BOX + 1) & ~1);  // 16-byte aligned
   for (int i = threadIdx.x; i < G1n; i += NTH) sgrp[i] = __ldg(&op.grp1[i]);
   for (int i = threadIdx.x; i < G1n * 12; i += NTH) stab[i] = __ldg(op.synth1 + i);
-  for (int i = threadIdx.x; i < op.G0 * 12; i += NTH) stab0[i] = __ldg(op.synth0 + i);
   constexpr int DEC = NTH - 1;
   const int64_t t0 = blockIdx.x, step = gridDim.x;
   if (threadIdx.x == DEC)
@@ -308,8 +335,8 @@ __global__ void __launch_bounds__(NTH, MINB)
     if (tile + 2 * step < n_tiles) tile3_prefetch_l2<NTH>(Hs[(it + 2) & 3], src);
     if (threadIdx.x == DEC && tile + 3 * step < n_tiles)
       tile3_decode(op, faces, tile + 3 * step, nch, align, u, Hs[(it + 3) & 3]);
-    if (H.narrow) tile3_phase_b<NTH, int>(H, op, dst, tr, stab, stab0, sgrp);
-    else tile3_phase_b<NTH, int64_t>(H, op, dst, tr, stab, stab0, sgrp);
+    if (H.narrow) tile3_phase_b<NTH, int>(H, op, dst, tr, stab, syn0, sgrp);
+    else tile3_phase_b<NTH, int64_t>(H, op, dst, tr, stab, syn0, sgrp);
   }
   cp_async_wait_all();
   raise_flag(flag, !isfinite(chk));

@@ -960,14 +960,16 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       if (align) b0 &= ~3, b1 = c + 1 < nch ? b1 & ~3 : u;
       cmax = std::max(cmax, b1 - b0);
     }
-    const size_t smem = 8 * (size_t(tile_box_offset(12, op->dev.G0, op->dev.G1)) + size_t(cmax) * (T3BOX + T3TP));
+    const size_t smem = 8 * (size_t(tile_box_offset(12, op->dev.G0, op->dev.G1)) + size_t((cmax * T3BOX + 1) & ~1) + size_t(cmax) * T3TP);
     const int64_t tiles = n_faces * int64_t(nch);
     if (smem <= 227 * 1024) {
       auto kfn = tile3_interp_kernel<288, 2>;
       int per_sm = 0;
       TH_CUDA(resident_ctas(reinterpret_cast<const void*>(kfn), 288, smem, &per_sm));
       const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));
-      kfn<<<tblocks, 288, smem, s>>>(op->dev, src, dst, faces, tiles, nch, align, cmax, u, flag);
+      T3Syn0 syn0;
+      std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
+      kfn<<<tblocks, 288, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, nch, align, cmax, u, flag);
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
