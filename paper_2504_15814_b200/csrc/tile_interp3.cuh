@@ -6,9 +6,10 @@
 // discrete Gram polynomials), organised so that no source load sits on a thread's
 // critical path and the normal / t1 passes are shared by every block that needs them:
 //
-//  * a CTA owns a tile = (face, chunk of <= 31 unknowns); the face's source support
-//    (5 normal x <= 7 x <= 7 coarse cells: the whole segment at p <= 9) is copied into
-//    a shared-memory box with 8-byte cp.async;
+//  * a CTA owns a tile = (face, spatial tile of <= 3 x 3 blocks, chunk of <= 31 unknowns);
+//    the tile's source support (5 normal x <= 7 x <= 7 coarse cells: the whole segment at
+//    p <= 9, a third of it per axis at p = 17) is copied into a shared-memory box with
+//    8-byte cp.async;
 //  * phase A, items (t2 slice z, unknown): the x (normal) Gram moments of the slice's
 //    <= 7 lines, then the y moments of each distinct t1 window start s (<= 3), written
 //    as T[s][z][pair] to a second shared region.  The box is then free: the NEXT
@@ -59,17 +60,24 @@ __device__ __forceinline__ int tile3_bound(int c, int nch, int u, int align) {
   return align ? (b & ~3) : b;
 }
 
+// tile = ((face, t2 tile, t1 tile), chunk): a face splits into nt x nt spatial tiles of <= 3 x 3
+// blocks (nt = 1 at p <= 9) and every spatial tile into nch chunks of unknowns
 __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __restrict__ faces, int64_t tile,
-                                             int nch, int align, int u, Tile3Hdr& H) {
-  const int64_t f = tile / nch;
-  const int c = int(tile - f * nch);
+                                             int nt, int nch, int align, int u, Tile3Hdr& H) {
+  const int64_t st = tile / nch;
+  const int c = int(tile - st * nch);
+  const int64_t f = st / (nt * nt);
+  const int tt = int(st - f * (nt * nt));
+  const int ti2 = tt / nt, ti1 = tt - ti2 * nt;
   FaceRef fr;
   decode_face(faces + f, op, fr);
+  const int a1 = ti1 * fr.n1 / nt, b1 = (ti1 + 1) * fr.n1 / nt;
+  const int a2 = ti2 * fr.n2 / nt, b2 = (ti2 + 1) * fr.n2 / nt;
   H.g0 = fr.g0;
-  H.g1 = fr.g1;
-  H.n1 = fr.n1;
-  H.g2 = fr.g2;
-  H.n2 = fr.n2;
+  H.g1 = fr.g1 + a1;
+  H.n1 = b1 - a1;
+  H.g2 = fr.g2 + a2;
+  H.n2 = b2 - a2;
   H.dst_off = fr.dst;
   H.sn = fr.sn;
   H.s1 = fr.s1;
@@ -300,7 +308,7 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
 template <int NTH, int MINB>
 __global__ void __launch_bounds__(NTH, MINB)
     tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
-                        const th_face* __restrict__ faces, int64_t n_tiles, int nch, int align, int cmax, int u,
+                        const th_face* __restrict__ faces, int64_t n_tiles, int nt, int nch, int align, int cmax, int u,
                         int32_t* flag) {
   static_assert(NTH == 32 * 9, "one warp per block of the 3 x 3 tile (phase B) and per t2 slice (phase A)");
   extern __shared__ __align__(16) double smem_t3[];
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   const int64_t t0 = blockIdx.x, step = gridDim.x;
   if (threadIdx.x == DEC)
     for (int i = 0; i < 3; ++i)
-      if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nch, align, u, Hs[i]);
+      if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nt, nch, align, u, Hs[i]);
   __syncthreads();
   if (t0 < n_tiles) tile3_fetch<NTH>(Hs[0], src, box);
   cp_async_commit();
@@ -334,7 +342,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     // the tile after next into L2, so that its copies above find it there one iteration later
     if (tile + 2 * step < n_tiles) tile3_prefetch_l2<NTH>(Hs[(it + 2) & 3], src);
     if (threadIdx.x == DEC && tile + 3 * step < n_tiles)
-      tile3_decode(op, faces, tile + 3 * step, nch, align, u, Hs[(it + 3) & 3]);
+      tile3_decode(op, faces, tile + 3 * step, nt, nch, align, u, Hs[(it + 3) & 3]);
     if (H.narrow) tile3_phase_b<NTH, int>(H, op, dst, tr, stab, syn0, sgrp);
     else tile3_phase_b<NTH, int64_t>(H, op, dst, tr, stab, syn0, sgrp);
   }

@@ -392,6 +392,7 @@ struct th_operator {
   int ti_mode = 0, ti_nt = 0;
   // staged order3 tile interpolation (tile_interp3.cuh) eligibility
   bool t3_ok = false;
+  int t3_nt = 1;
 };
 
 namespace {
@@ -546,8 +547,8 @@ void prepare_tile(th_operator* op) {
 
 // Staged order3 tile interpolation eligibility (tile_interp3.cuh): one normal group with a
 // 5-cell window and <= 3 children; tangential groups with 5-cell windows, <= 3 children and
-// non-decreasing starts; every segment axis holds <= 3 groups whose windows span <= T3Y
-// cells (one tile per face: p <= 9).
+// non-decreasing starts; every segment axis splits into t3_nt balanced runs of <= 3 groups
+// whose windows span <= T3Y cells (one run at p <= 9, three at p = 17).
 void prepare_tile3(th_operator* op) {
   const th::HostOperator& h = op->host;
   op->t3_ok = false;
@@ -561,11 +562,19 @@ void prepare_tile3(th_operator* op) {
     if (g1[j].winL != 5 || g1[j].tgtN < 1 || g1[j].tgtN > 3) return;
     if (j > 0 && g1[j].win0 < g1[j - 1].win0) return;
   }
+  int nmax = 0;
+  for (int c = 0; c < 3; ++c) nmax = std::max(nmax, h.seg_g[c][1] - h.seg_g[c][0]);
+  if (nmax < 1) return;
+  const int nt = (nmax + 2) / 3;  // spatial tiles per face axis: <= 3 groups each
   for (int c = 0; c < 3; ++c) {
-    const int a = h.seg_g[c][0], n = h.seg_g[c][1] - a;
-    if (n > 3) return;
-    if (n > 0 && g1[a + n - 1].win0 + 5 - g1[a].win0 > T3Y) return;
+    const int a0 = h.seg_g[c][0], n = h.seg_g[c][1] - a0;
+    for (int t = 0; t < nt; ++t) {
+      const int a = a0 + t * n / nt, b = a0 + (t + 1) * n / nt;
+      if (b - a > 3) return;
+      if (b > a && g1[b - 1].win0 + 5 - g1[a].win0 > T3Y) return;
+    }
   }
+  op->t3_nt = nt;
   op->t3_ok = true;
 }
 
@@ -946,7 +955,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   //   TH_TILE3=0                 order3 interpolation through the per-warp slide instead of the
   //                              staged two-phase tiles (tile_interp3.cuh)
   static const int use_tile3 = [] { const char* e = std::getenv("TH_TILE3"); return e ? std::atoi(e) : 1; }();
-  if (use_tile3 && interp && op->t3_ok && !stage_interp) {
+  //   TH_TILE3=2                 also when a face splits into several spatial tiles (p = 17)
+  if (use_tile3 && interp && op->t3_ok && !stage_interp && (op->t3_nt == 1 || use_tile3 == 2)) {
     // tiles = (face, chunk of <= T3CMAX unknowns); chunk boundaries on 4-unknown (32-byte)
     // sector edges when every chunk still fits
     const int nch = (u + T3CMAX - 1) / T3CMAX;
@@ -961,7 +971,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       cmax = std::max(cmax, b1 - b0);
     }
     const size_t smem = 8 * (size_t(tile_box_offset(12, op->dev.G0, op->dev.G1)) + size_t((cmax * T3BOX + 1) & ~1) + size_t(cmax) * T3TP);
-    const int64_t tiles = n_faces * int64_t(nch);
+    const int nt = op->t3_nt;
+    const int64_t tiles = n_faces * int64_t(nt * nt * nch);
     if (smem <= 227 * 1024) {
       auto kfn = tile3_interp_kernel<288, 2>;
       int per_sm = 0;
@@ -969,7 +980,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));
       T3Syn0 syn0;
       std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
-      kfn<<<tblocks, 288, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, nch, align, cmax, u, flag);
+      kfn<<<tblocks, 288, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, nt, nch, align, cmax, u, flag);
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
