@@ -137,6 +137,24 @@ __device__ __forceinline__ void tile_fetch(const TileHdr& H, const double* __res
   }
 }
 
+// L2 prefetch of a tile's source box (the tile after next, so that its cp.async copies one
+// iteration later find it in L2): one (cell, 128-byte line) per thread and iteration
+template <int NTH>
+__device__ __forceinline__ void tile_prefetch_l2(const TileHdr& H, const double* __restrict__ src, int u) {
+  const int ny = H.ny, n = 3 * ny * H.nz;
+  if (H.cnt <= 0) return;
+  const int nl = (u * 8 + 127) / 128 + 1;  // lines a u-double cell can touch (8-byte alignment)
+  const int last = u * 8 - 1;
+  const char* const base = reinterpret_cast<const char*>(src + H.src_off);
+#pragma unroll 1
+  for (int c = threadIdx.x; c < n * nl; c += NTH) {
+    const int cell = c / nl, part = c - cell * nl;
+    const int x = cell % 3, r = cell / 3, z = r / ny, y = r - z * ny;
+    const char* const pc = base + 8 * (int64_t(x) * H.sn + int64_t(y) * H.s1 + int64_t(z) * H.s2);
+    l2_prefetch_line(pc + min(part * 128, last));
+  }
+}
+
 // one item: 3 x 3 x 3 window -> 27 children.  ALL: every child is a target (always at p = 9).
 template <bool TENSOR, bool ALL, typename OFF>
 __device__ __forceinline__ void tile_item(const double* w, const double* r0, const double* r1, const double* r2,
@@ -308,7 +326,7 @@ __global__ void __launch_bounds__(NTH, MINB)
                        int32_t* flag) {
   constexpr int TW = TENSOR ? 9 : 12;
   extern __shared__ __align__(16) double smem_tile[];
-  __shared__ TileHdr Hs[3];  // tiles it (computing), it + 1 (fetching), it + 2 (decoding)
+  __shared__ TileHdr Hs[4];  // tiles it (computing), it + 1 (fetching), it + 2 (L2 prefetch), it + 3 (decoding)
   const int G1n = op.G1;
   int4* const sgrp = reinterpret_cast<int4*>(smem_tile);
   double* const stab = smem_tile + 2 * G1n;
@@ -332,22 +350,24 @@ __global__ void __launch_bounds__(NTH, MINB)
   // the decoding thread is the last one: it has the fewest items when a tile does not divide evenly
   constexpr int DEC = NTH - 1;
   const int64_t t0 = blockIdx.x, step = gridDim.x;
-  if (threadIdx.x == DEC) {
-    if (t0 < n_tiles) tile_decode(op, faces, t0, nt, u, Hs[0]);
-    if (t0 + step < n_tiles) tile_decode(op, faces, t0 + step, nt, u, Hs[1]);
-  }
+  const bool pf = op.prefetch & 16;  // TH_PREFETCH bit 16: L2 prefetch of the tile after next
+  if (threadIdx.x == DEC)
+    for (int i = 0; i < 3; ++i)
+      if (t0 + i * step < n_tiles) tile_decode(op, faces, t0 + i * step, nt, u, Hs[i]);
   __syncthreads();
   if (t0 < n_tiles) tile_fetch<NTH>(Hs[0], src, boxes, pitch, u);
   cp_async_commit();
+  if (pf && t0 + step < n_tiles) tile_prefetch_l2<NTH>(Hs[1], src, u);
   double chk = 0.0;  // fma(T0, 0, chk) stays 0 for finite inputs, turns NaN for any Inf / NaN
   int it = 0;
   for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
     cp_async_wait_all();
     __syncthreads();  // this tile's box landed; the previous tile's compute is done with the other box
-    if (tile + step < n_tiles) tile_fetch<NTH>(Hs[(it + 1) % 3], src, boxes + ((it + 1) & 1) * box_doubles, pitch, u);
+    if (tile + step < n_tiles) tile_fetch<NTH>(Hs[(it + 1) & 3], src, boxes + ((it + 1) & 1) * box_doubles, pitch, u);
     cp_async_commit();
-    if (threadIdx.x == DEC && tile + 2 * step < n_tiles) tile_decode(op, faces, tile + 2 * step, nt, u, Hs[(it + 2) % 3]);
-    const TileHdr& H = Hs[it % 3];
+    if (pf && tile + 2 * step < n_tiles) tile_prefetch_l2<NTH>(Hs[(it + 2) & 3], src, u);
+    if (threadIdx.x == DEC && tile + 3 * step < n_tiles) tile_decode(op, faces, tile + 3 * step, nt, u, Hs[(it + 3) & 3]);
+    const TileHdr& H = Hs[it & 3];
     const double* box = boxes + (it & 1) * box_doubles;
     if (H.narrow) tile_compute<TENSOR, NTH, int>(H, op, dst, box, pitch, stab, stab0, sgrp, u, umag, chk);
     else tile_compute<TENSOR, NTH, int64_t>(H, op, dst, box, pitch, stab, stab0, sgrp, u, umag, chk);

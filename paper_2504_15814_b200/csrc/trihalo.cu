@@ -729,7 +729,9 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   d.n_blocks = (int32_t)h.block_off.size();
   {
     const char* e = std::getenv("TH_PREFETCH");
-    d.prefetch = e ? std::atoi(e) : 9;  // bit 1: restriction window bulk prefetch, bit 8: interp unit windows
+    // bit 1: restriction window bulk prefetch, bit 8: interp unit windows, bit 16: staged tile
+    // interpolation prefetches the tile after next (profiles/r01_ab_tile3.txt)
+    d.prefetch = e ? std::atoi(e) : 25;
   }
   d.units_per_face = 0;
   d.ns_t = h.ax[1].ns;
