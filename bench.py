@@ -37,6 +37,7 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="shrink patch / face counts (tuning runs only)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-chunks", type=int, default=16, help="pipeline chunks of the e2e leg")
     ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -440,7 +441,7 @@ def run_e2e(args, wl, passes, dev, world):
         lo, cnt = ps["batch"].op.support_layers()
         a, b = layers.get(ps["role"], (lo, lo + cnt))
         layers[ps["role"]] = (min(a, lo), max(b, lo + cnt))
-    n_chunks = 8
+    n_chunks = max(1, args.e2e_chunks)
     outs_d = [torch.empty(ps["out"].numel(), dtype=torch.float64, device=dev) for ps in passes]
     outs_h = [torch.empty(ps["out"].numel(), dtype=torch.float64, pin_memory=True) for ps in passes]
     chunks = []
@@ -530,7 +531,7 @@ def run_e2e(args, wl, passes, dev, world):
             "ms_per_step": round(t_step * 1e3, 2), "matches_device_run": agree,
             "how": "pinned host buffers of the per-face reference source layouts -> only the operators' normal "
                    "support layers shipped (th_copy_box_layers, strided 2D/3D async copies) -> th_apply_faces -> "
-                   "pinned host outputs; 8 chunks pipelined over copy/compute/copy streams; wall clock with "
+                   "pinned host outputs; 16 chunks pipelined over copy/compute/copy streams; wall clock with "
                    "device sync"}
 
 
