@@ -200,7 +200,9 @@ def test_pool_interp_unknown_counts(th, scheme, p, u):
     """Interpolation across unknown counts: the staged tile kernel's flattened (block, unknown)
     items and its [unknown][cell] box at u = 1 (one item per block), 33 / 65 (items straddling
     warps), 130 (a 156 KB box pair: one CTA per SM), 200 (boxes beyond shared memory: the
-    per-warp slide takes over); the slide's ragged 32-unknown chunks."""
+    per-warp slide takes over); the slide's ragged 32-unknown chunks; for order3 the two-phase
+    tiles' chunks of <= 31 unknowns, on 4-unknown sector boundaries (33, 65, 130) or not (200:
+    aligned boundaries would leave a 32-unknown chunk)."""
     import torch
 
     k = 3
