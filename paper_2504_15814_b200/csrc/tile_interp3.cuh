@@ -8,16 +8,18 @@
 //
 //  * a CTA owns a tile = (face, spatial tile of <= 3 x 3 blocks, chunk of <= 31 unknowns);
 //    the tile's source support (5 normal x <= 7 x <= 7 coarse cells: the whole segment at
-//    p <= 9, a third of it per axis at p = 17) is copied into a shared-memory box with
-//    8-byte cp.async;
-//  * phase A, items (t2 slice z, unknown): the x (normal) Gram moments of the slice's
-//    <= 7 lines, then the y moments of each distinct t1 window start s (<= 3), written
-//    as T[s][z][pair] to a second shared region.  The box is then free: the NEXT
+//    p <= 9; with TH_TILE3=2 a third of it per axis at p = 17) is copied into a
+//    shared-memory box with 8-byte cp.async, and the tile after next is L2-prefetched;
+//  * phase A, warp = t2 slice z, lane = unknown: the x (normal) Gram moments of the
+//    slice's <= 7 lines, then the y moments of each distinct t1 window start s (<= 3),
+//    written as T[s][z][pair] to a second shared region.  The box is then free: the NEXT
 //    tile's copy is issued before phase B, so it lands while phase B computes;
-//  * phase B, items (block, unknown) with the unknown fastest: the block's z moments
-//    from its 5 T slices, the synthesis at its <= 27 children, direct stores (a warp
-//    writes contiguous runs of unknowns).
-// Two CTAs per SM (2 x 114 KB of shared memory) alternate between the phases.
+//  * phase B, warp = block, lane = unknown: the block's z moments from its 5 T slices,
+//    the synthesis at its <= 27 children, direct stores (a warp writes contiguous runs of
+//    unknowns).
+// Two CTAs per SM (2 x 114 KB of shared memory) alternate between the phases; that
+// interleaving is what hides the barriers (one 18-warp CTA per SM measured 0.43 of HBM
+// against 0.58, profiles/r01_ab_tile3.txt).
 #pragma once
 
 constexpr int T3Y = 7;                    // box extent along t1 / t2 (three 5-cell windows within 7 cells)
@@ -303,8 +305,8 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
   }
 }
 
-// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (unused [G0][12]) | box[cmax][T3BOX] (+1 to an
-// even count) | T[cmax][T3TP]
+// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (a [G0][12] slot, unused here: the
+// normal table is the kernel parameter syn0) | box[cmax][T3BOX] (+1 to an even count) | T[cmax][T3TP]
 template <int NTH, int MINB>
 __global__ void __launch_bounds__(NTH, MINB)
     tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
