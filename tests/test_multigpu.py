@@ -1,5 +1,5 @@
 """Multi-GPU layer host logic on CPU: partition, ownership plan and the grouped
-P2P exchange, world_size 2 over gloo (the kernels are replaced by a stamp so
+P2P exchange, world sizes 2 and 4 over gloo (the kernels are replaced by a stamp so
 the bookkeeping is checked exactly)."""
 
 from __future__ import annotations
@@ -91,11 +91,14 @@ def _free_port():
     return port
 
 
-def test_sweep_exchange_world2_gloo():
+@pytest.mark.parametrize("world", (2, 4))
+def test_sweep_exchange_gloo(world):
+    """The grouped P2P exchange of cross faces over gloo at world size 2 and 4 (every rank
+    sends to and receives from several peers in one batch)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
