@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--overlap", action="store_true", help="A/B: interpolation passes on a side stream (diagnosis)")
     ap.add_argument("--reverse-passes", action="store_true", help="run the step's passes in reverse order (diagnosis)")
     return ap.parse_args()
 
@@ -175,8 +176,20 @@ def run_ours(args, rank, world, local_rank):
                            values=ids.size * n_tgt * u, bytes=b * ids.size + op.info.device_bytes,
                            flops=f * ids.size))
     stream = torch.cuda.current_stream()
+    side = torch.cuda.Stream(device=dev) if args.overlap else None
 
     def step(evs=None):
+        if side is not None:  # A/B: interpolation passes on a side stream beside the restrictions
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                for ps in passes:
+                    if ps["role"] == "interpolate":
+                        ps["batch"].launch(ps["src"], ps["out"], stream=side.cuda_stream, check_flag=False)
+            for ps in passes:
+                if ps["role"] != "interpolate":
+                    ps["batch"].launch(ps["src"], ps["out"], check_flag=False)
+            stream.wait_stream(side)
+            return
         for i, ps in enumerate(passes):
             if evs is not None:
                 evs[i].record(stream)
@@ -208,6 +221,14 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     clocks = sampler.stop()
     total_ms = t0.elapsed_time(t1)
+    if side is not None:  # no per-pass events in the overlapped step: one serial step per pass row
+        ev_all = ev_all[:1]
+        step(None)
+        torch.cuda.synchronize()
+        side_, side = side, None
+        step(ev_all[0])
+        side = side_
+        torch.cuda.synchronize()
     per_pass_ms = [statistics.mean(ev[i].elapsed_time(ev[i + 1]) for ev in ev_all) for i in range(len(passes))]
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -234,7 +255,8 @@ def run_ours(args, rank, world, local_rank):
                    "layout": "coarse pool (p+2k)^3 AoS + per-face fine restriction slabs (world layout)",
                    "l2": f"inputs {(wl.pool.numel() + (wl.fine.numel() if wl.fine is not None else 0)) * 8 / 1e9:.1f} GB"
                          " >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"weak: {world} independent shard(s)"},
+                   "parallelism": f"weak: {world} independent shard(s)",
+                   **({"overlap": "interpolation passes on a side stream"} if args.overlap else {})},
         "roofline": {"bound": "hbm", "kernel": f"{passes[dom]['role']}:{passes[dom]['scheme']}",
                      "achieved": pass_rows[dom]["alg_GBps"], "peak": peak, "unit": "GB/s",
                      "frac": round(pass_rows[dom]["alg_GBps"] / peak, 4), "traffic": None,
