@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-same-level", action="store_true", help="skip the same-level halo fill leg")
     ap.add_argument("--overlap", action="store_true", help="A/B: interpolation passes on a side stream (diagnosis)")
     ap.add_argument("--reverse-passes", action="store_true", help="run the step's passes in reverse order (diagnosis)")
     return ap.parse_args()
@@ -283,7 +284,54 @@ def run_ours(args, rank, world, local_rank):
         result["e2e"] = run_e2e(args, wl, passes, dev, world)
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"], result["parity"] = cpu_baseline(args, wl, passes)
+    if not args.no_same_level:  # last: it rewrites the pool's halos
+        result["same_level"] = same_level_leg(wl, dev, peak)
     return result
+
+
+def same_level_leg(wl, dev, peak, reps=20):
+    """Same-level halo fill (th_copy_faces) over the workload's patch pool:
+    all six faces of every patch from a random same-level neighbour, bit-exactness of a
+    sample checked against the copy, k x p x p cells x u read + written per face."""
+    import numpy as np
+    import torch
+
+    import paper_2504_15814_b200 as th
+
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    n = wl.pool.numel() // ((p + 2 * k) ** 3 * u)
+    rng = np.random.default_rng(100 + s.config)
+    dst = np.repeat(np.arange(n), 6)
+    nrm, sid = np.tile(np.repeat(np.arange(3), 2), n), np.tile(np.arange(2), 3 * n)
+    src = (dst + rng.integers(1, max(n, 2), dst.size)) % max(n, 2) if n > 1 else dst
+    rec = th.pool_same_level_faces(p, k, u, src, dst, nrm, sid)
+    rec_d = torch.from_numpy(rec.view(np.uint8).ravel().copy()).to(dev)
+    pool = wl.pool
+    for _ in range(3):
+        th.copy_faces(pool, pool, rec_d, k, p, u)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        th.copy_faces(pool, pool, rec_d, k, p, u)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    byts = 2 * dst.size * k * p * p * u * 8
+    # sample: face 0's halo box equals its neighbour's interior box
+    E = p + 2 * k
+    v = pool.view(n, E, E, E, u)
+    r0 = rec[0]
+    ax = 2 - int(r0["normal"])
+    a = [slice(k, k + p)] * 3
+    b = list(a)
+    a[ax] = slice(p, p + k) if r0["side"] == 0 else slice(k, 2 * k)
+    b[ax] = slice(0, k) if r0["side"] == 0 else slice(p + k, p + 2 * k)
+    ok = bool(torch.equal(v[(int(src[0]), *a)], v[(int(dst[0]), *b)]))
+    gbs = byts / (ms / 1e3) / 1e9
+    return {"faces": int(dst.size), "ms": round(ms, 4), "alg_bytes": int(byts), "alg_GBps": round(gbs, 1),
+            "frac_hbm": round(gbs / peak, 3), "sample_bit_exact": ok, "launches": reps}
 
 
 def run_multi(args, rank, world, local_rank):

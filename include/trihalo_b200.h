@@ -20,6 +20,8 @@
  *   th_operator_export_rows  CsrOperator rows of a segment / half row block
  *                            (csr.py:176-248), for parity checks and dumps.
  *   th_scheme_feasible       scheme_feasible (schemes.py:23-47).
+ *   th_copy_faces            same-level halo fill between patches of one level
+ *                            (outside the reference).
  *
  * Conventions
  *   - Cell data are AoS: the u unknowns of a cell are contiguous (stride 1),
@@ -159,6 +161,16 @@ int32_t th_operator_support_layers(const th_operator* op, int32_t* lo, int32_t* 
  * from host buffers in the reference layout. */
 int32_t th_copy_box_layers(const double* src, double* dst, int64_t n_faces, int32_t normal, int32_t n_ext,
                            int32_t t_ext, int32_t u, int32_t lo, int32_t count, int32_t kind, void* stream);
+
+/* Same-level halo copy (no reference counterpart: the reference
+ * handles 3:1 faces only, so this is the part of a time step's halo fill between two
+ * patches of the same level).  Face f copies the n_ext x t_ext x t_ext world box of
+ * cells (n_ext along faces[f].normal) at src + faces[f].src[0] (world strides
+ * faces[f].src_stride) to dst + faces[f].dst (strides faces[f].dst_stride), u unknowns
+ * per cell, unknown stride 1.  Bit-exact copy; src and dst may be the same pool when
+ * the boxes do not overlap.  All pointers device. */
+int32_t th_copy_faces(const double* src, double* dst, const th_face* faces, int64_t n_faces, int32_t n_ext,
+                      int32_t t_ext, int32_t u, void* stream);
 
 /* CSR apply on reference-frame AoS buffers (csr.py:143-173); all pointers device. */
 int32_t th_csr_apply(const int64_t* row_offsets, const int64_t* col_indices, const double* values,

@@ -174,3 +174,23 @@ def subregion_rows(full: Region, sub: Region) -> np.ndarray:
     fx, fy, _ = full.extents
     rows = ((k2 + sh[2]) * fy + (j + sh[1])) * fx + (i + sh[0])
     return rows.ravel().astype(np.int64)
+
+
+def same_level_fill(pool: np.ndarray, p: int, k: int, src_ids, dst_ids, normals, sides) -> np.ndarray:
+    """Same-level halo fill of a patch pool (the reference has no
+    counterpart — it handles 3:1 faces only — so this restates the plain copy in world
+    (z, y, x, u) grids, geometry.py:26-30 ordering).  ``pool`` is (n, E, E, E, u) with
+    E = p + 2k; returns a filled copy.  Face i: side 0 -> halo normal layers [0, k) of
+    dst <- interior [p, p + k) of src; side 1 -> halo [p + k, p + 2k) <- interior [k, 2k);
+    tangential interior [k, k + p) only."""
+    out = pool.copy()
+    for s, d, nrm, sd in zip(src_ids, dst_ids, normals, sides):
+        src_n = slice(p, p + k) if sd == 0 else slice(k, 2 * k)
+        dst_n = slice(0, k) if sd == 0 else slice(p + k, p + 2 * k)
+        tan = slice(k, k + p)
+        ax = 2 - int(nrm)  # world axis x/y/z -> grid axis 2/1/0
+        src_idx = [tan, tan, tan]
+        dst_idx = [tan, tan, tan]
+        src_idx[ax], dst_idx[ax] = src_n, dst_n
+        out[(int(d), *dst_idx)] = pool[(int(s), *src_idx)]
+    return out

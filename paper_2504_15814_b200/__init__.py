@@ -45,7 +45,7 @@ from .schemes import (
     restrict_halo,
     scheme_feasible,
 )
-from .faces import FaceBatch, pool_interp_faces, pool_restrict_faces, slab_faces
+from .faces import FaceBatch, copy_faces, pool_interp_faces, pool_restrict_faces, pool_same_level_faces, slab_faces
 from .csrio import dump_operator, dumps_operator, extract_half, extract_segment, from_triplets, load_operator
 from .harness import (
     BenchReport,

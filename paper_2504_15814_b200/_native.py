@@ -58,7 +58,7 @@ EXPORTED = (
     "th_abi_version", "th_last_error", "th_last_error_column", "th_scheme_feasible", "th_operator_create",
     "th_operator_create_host",
     "th_operator_destroy", "th_operator_info_get", "th_operator_export_rows", "th_apply_faces",
-    "th_check_finite", "th_csr_apply", "th_operator_support_layers", "th_copy_box_layers",
+    "th_check_finite", "th_csr_apply", "th_operator_support_layers", "th_copy_box_layers", "th_copy_faces",
 )
 
 _lib = None
@@ -104,6 +104,8 @@ def load():
     lib.th_operator_support_layers.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
     lib.th_copy_box_layers.restype = _i32
     lib.th_copy_box_layers.argtypes = [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp]
+    lib.th_copy_faces.restype = _i32
+    lib.th_copy_faces.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp]
     lib.th_csr_apply.restype = _i32
     lib.th_csr_apply.argtypes = [_vp, _vp, _vp, _i64, _vp, _vp, _i32, _vp]
     _lib = lib

@@ -25,6 +25,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
+from .errors import ContractViolationError
 from .geometry import half_layers
 
 FACE_DTYPE = _native.FACE_DTYPE
@@ -167,6 +168,48 @@ def pool_restrict_faces(p: int, k: int, u: int, fine_ids, normals, sides, half=N
         d_start = np.where(sides == 0, p + k + lo, k - hi)
         rec["dst"] = coarse_ids * patch + _corner(normals, d_start, k, strides)
     return rec
+
+
+def pool_same_level_faces(p: int, k: int, u: int, src_ids, dst_ids, normals, sides) -> np.ndarray:
+    """Same-level halo faces of the patch pool.
+
+    Face i fills the k halo layers of patch ``dst_ids[i]`` on its face (``normals[i]``,
+    ``sides[i]``) from the k interior layers of the same-level neighbour ``src_ids[i]``
+    next to the shared face, over the p x p tangential interior (pool layout as in
+    ``pool_geometry``).  ``sides[i]`` = 0: the neighbour is on the destination's negative
+    side, so halo normal layers [0, k) <- neighbour interior [p, p + k); 1: halo
+    [p + k, p + 2k) <- neighbour interior [k, 2k).  Apply with ``copy_faces(pool, pool,
+    rec, k, p, u)``; the boxes never overlap (halo vs interior cells).
+    """
+    normals = np.asarray(normals, dtype=np.int64).ravel()
+    sides = np.asarray(sides, dtype=np.int64).ravel()
+    src_ids = np.asarray(src_ids, dtype=np.int64).ravel()
+    dst_ids = np.asarray(dst_ids, dtype=np.int64).ravel()
+    n = normals.size
+    _, patch, strides = pool_geometry(p, k, u)
+    rec = _records(n)
+    rec["normal"], rec["side"] = normals, sides
+    rec["src"][:, 0] = src_ids * patch + _corner(normals, np.where(sides == 0, p, k), k, strides)
+    rec["dst"] = dst_ids * patch + _corner(normals, np.where(sides == 0, 0, p + k), k, strides)
+    rec["src_stride"] = strides
+    rec["dst_stride"] = strides
+    return rec
+
+
+def copy_faces(src, dst, records, n_ext: int, t_ext: int, u: int, stream=None) -> None:
+    """Launch ``th_copy_faces`` over face records (numpy records or a device uint8 tensor
+    holding them): each face copies an n_ext x t_ext x t_ext world box of cells."""
+    import torch
+
+    lib = _native.load()
+    if isinstance(records, np.ndarray):
+        records = torch.from_numpy(records.view(np.uint8).ravel().copy()).to(src.device)
+    n = records.numel() // _native.FACE_DTYPE.itemsize
+    for t in (src, dst):
+        if not (t.is_cuda and t.dtype == torch.float64):
+            raise ContractViolationError("copy_faces needs float64 CUDA tensors")
+    s = torch.cuda.current_stream(src.device).cuda_stream if stream is None else stream
+    _native.check(lib.th_copy_faces(src.data_ptr(), dst.data_ptr(), records.data_ptr(), n, n_ext, t_ext, u, s))
 
 
 class FaceBatch:
