@@ -1045,50 +1045,64 @@ int32_t th_check_finite(const double* values, int64_t n, int32_t* flag, void* st
 
 // Same-level halo copy: each face record moves an n_ext x t_ext x t_ext
 // world box of cells from src[0] to dst, both addressed through their world strides.  Work
-// unit = one warp per x-run of the box (n_ext cells when the normal is x, t_ext otherwise):
-// with the patch pool's strides a run is one contiguous span of cells * u doubles in both
-// source and target, streamed with coalesced 8-byte loads (cells are 8-byte aligned only).
+// unit = one warp per (face, quarter of the box's values); the warp reads the face record once
+// and streams its quarter as x-runs (n_ext cells when the normal is x, t_ext otherwise), which
+// with the pool's strides are contiguous spans of cells * u doubles in source and target.
+// Four 8-byte loads in flight per lane, positions advanced incrementally (no divisions per
+// value).  The first version (warp per x-run, record re-read per run) was latency bound at
+// 0.77-0.80 of the copy peak: three dependent record loads per 4 KB moved.
+constexpr int kCopyChunks = 4;
+
 __global__ void __launch_bounds__(256) box_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                                        const th_face* __restrict__ faces, int64_t n_faces,
                                                        int n_ext, int t_ext, int u) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; ; w += nw) {
-    // rows (y, z) per face: t_ext^2 when the normal is x, n_ext * t_ext otherwise; rows are
-    // numbered with a fixed per-face stride (the larger count) and the excess skipped
-    const int64_t stride = int64_t(n_ext > t_ext ? n_ext : t_ext) * t_ext;
-    const int64_t f = w / stride;
-    if (f >= n_faces) break;
-    const th_face* fp = faces + f;
+  const int64_t units = n_faces * kCopyChunks;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < units; w += nw) {
+    const th_face* fp = faces + w / kCopyChunks;
+    const int c = int(w % kCopyChunks);
     const int normal = __ldg(&fp->normal);
     const int ext_x = normal == 0 ? n_ext : t_ext;
     const int ext_y = normal == 1 ? n_ext : t_ext;
     const int ext_z = normal == 2 ? n_ext : t_ext;
-    const int64_t r = w - f * stride;
-    if (r >= int64_t(ext_y) * ext_z) continue;
-    const int y = int(r % ext_y), z = int(r / ext_y);
-    const int64_t so = __ldg(&fp->src[0]) + y * __ldg(&fp->src_stride[1]) + z * __ldg(&fp->src_stride[2]);
-    const int64_t dof = __ldg(&fp->dst) + y * __ldg(&fp->dst_stride[1]) + z * __ldg(&fp->dst_stride[2]);
-    const int64_t sx = __ldg(&fp->src_stride[0]), dx = __ldg(&fp->dst_stride[0]);
-    if (sx == u && dx == u) {  // contiguous run
-      const int n = ext_x * u;
-      const double* s = src + so;
-      double* d = dst + dof;
-      // four loads in flight per lane before the stores (one per lane left the kernel
-      // latency bound: long_scoreboard 31 stalls per issue at 0.80 of the copy peak)
-      for (int j = lane; j < n; j += 128) {
+    const int64_t s0 = __ldg(&fp->src[0]), d0 = __ldg(&fp->dst);
+    const int64_t sx = __ldg(&fp->src_stride[0]), sy = __ldg(&fp->src_stride[1]), sz = __ldg(&fp->src_stride[2]);
+    const int64_t dx = __ldg(&fp->dst_stride[0]), dy = __ldg(&fp->dst_stride[1]), dz = __ldg(&fp->dst_stride[2]);
+    const int n = ext_x * u;                       // values per x-run
+    const int64_t total = int64_t(n) * ext_y * ext_z;
+    const int64_t beg = total * c / kCopyChunks, end = total * (c + 1) / kCopyChunks;
+    if (sx == u && dx == u) {
+      // position of value e = beg + lane as (run r, offset j); runs are (y, z) with y fastest
+      int64_t e = beg + lane;
+      int64_t r = e / n;
+      int j = int(e - r * n);
+      int y = int(r % ext_y), z = int(r / ext_y);
+      while (e < end) {
         double v[4];
+        int64_t so[4], dof[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          so[i] = s0 + y * sy + z * sz + j;
+          dof[i] = d0 + y * dy + z * dz + j;
+          if (e + 32 * i < end) v[i] = __ldg(src + so[i]);
+          j += 32;  // advance to this lane's next value
+          while (j >= n) {
+            j -= n;
+            if (++y == ext_y) { y = 0; ++z; }
+          }
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (j + 32 * i < n) v[i] = __ldg(s + j + 32 * i);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (j + 32 * i < n) d[j + 32 * i] = v[i];
+          if (e + 32 * i < end) dst[dof[i]] = v[i];
+        e += 128;
       }
-    } else {
-      for (int j = lane; j < ext_x * u; j += 32) {
-        const int c = j / u, q = j - c * u;
-        dst[dof + c * dx + q] = __ldg(src + so + c * sx + q);
+    } else {  // general strides: value e -> (run, cell, unknown)
+      for (int64_t e = beg + lane; e < end; e += 32) {
+        const int64_t r = e / n;
+        const int j = int(e - r * n), cell = j / u, q = j - cell * u;
+        const int y = int(r % ext_y), z = int(r / ext_y);
+        dst[d0 + y * dy + z * dz + cell * dx + q] = __ldg(src + s0 + y * sy + z * sz + cell * sx + q);
       }
     }
   }
@@ -1100,8 +1114,8 @@ int32_t th_copy_faces(const double* src, double* dst, const th_face* faces, int6
   if (n_faces == 0) return TH_OK;
   if (!src || !dst || !faces) return fail(TH_ERR_CONTRACT, "NULL source, target or face pointer");
   if (n_ext < 1 || t_ext < 1 || u < 1) return fail(TH_ERR_CONFIG, "box extents and u must be >= 1");
-  const int64_t rows = int64_t(std::max(n_ext, t_ext)) * t_ext * n_faces;  // one warp each
-  const int blocks = int(std::min<int64_t>((rows + 7) / 8, int64_t(num_sms()) * 8));
+  const int64_t units = n_faces * kCopyChunks;  // one warp each
+  const int blocks = int(std::min<int64_t>((units + 7) / 8, int64_t(num_sms()) * 8));
   box_copy_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, faces, n_faces, n_ext, t_ext, u);
   TH_CUDA(cudaGetLastError());
   return TH_OK;

@@ -94,3 +94,31 @@ def test_copy_faces_empty_and_errors():
         th.copy_faces(d, d, th.pool_same_level_faces(5, 2, 1, [0], [1], [0], [0]), 0, 5, 1)
     with pytest.raises(th.ContractViolationError):
         th.copy_faces(d.float(), d, th.pool_same_level_faces(5, 2, 1, [0], [1], [0], [0]), 2, 5, 1)
+
+
+@pytest.mark.gpu
+def test_copy_faces_general_strides():
+    """Target cells spaced two cells apart along x (not a contiguous run): the general path."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_15814_b200 as th
+
+    p, k, u = 5, 2, 3
+    E = p + 2 * k
+    rng = np.random.default_rng(7)
+    pool = rng.standard_normal((2, E, E, E, u))
+    for normal in range(3):
+        rec = th.pool_same_level_faces(p, k, u, [0], [1], [normal], [1])
+        ext = [p, p, p]
+        ext[normal] = k
+        rec["dst"] = 0
+        rec["dst_stride"] = [2 * u, 2 * u * ext[0], 2 * u * ext[0] * ext[1]]
+        out = torch.zeros(2 * u * ext[0] * ext[1] * ext[2], dtype=torch.float64, device="cuda")
+        th.copy_faces(torch.from_numpy(pool.ravel().copy()).cuda(), out, rec, k, p, u)
+        got = out.cpu().numpy().reshape(ext[2], ext[1], ext[0], 2, u)[:, :, :, 0]
+        idx = [slice(k, k + p)] * 3
+        idx[2 - normal] = slice(k, 2 * k)
+        assert np.array_equal(got, pool[(0, *idx)])
+        assert not out.cpu().numpy().reshape(ext[2], ext[1], ext[0], 2, u)[:, :, :, 1].any()
