@@ -1045,13 +1045,13 @@ int32_t th_check_finite(const double* values, int64_t n, int32_t* flag, void* st
 
 // Same-level halo copy: each face record moves an n_ext x t_ext x t_ext
 // world box of cells from src[0] to dst, both addressed through their world strides.  Work
-// unit = one warp per (face, quarter of the box's values); the warp reads the face record once
-// and streams its quarter as x-runs (n_ext cells when the normal is x, t_ext otherwise), which
+// unit = one warp per (face, eighth of the box's values); the warp reads the face record once
+// and streams its eighth as x-runs (n_ext cells when the normal is x, t_ext otherwise), which
 // with the pool's strides are contiguous spans of cells * u doubles in source and target.
 // Four 8-byte loads in flight per lane, positions advanced incrementally (no divisions per
 // value).  The first version (warp per x-run, record re-read per run) was latency bound at
 // 0.77-0.80 of the copy peak: three dependent record loads per 4 KB moved.
-constexpr int kCopyChunks = 4;
+constexpr int kCopyChunks = 8;
 
 __global__ void __launch_bounds__(256) box_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                                        const th_face* __restrict__ faces, int64_t n_faces,
