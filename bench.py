@@ -3,10 +3,13 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 A step is one pass of every (role, scheme) of BASELINE.json's config over all
-of its faces, inputs resident in HBM.  Default: config 2 (configs[1]): p=9,
-k=3, u=59, 1,024 coarse patches, 4,096 faces; tensor_linear + order2
-interpolation and tensor_linear + order2 restriction (full coarse face) of
-every face.  Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement.
+of its faces, inputs resident in HBM.  Default: config 5 (configs[4]), the
+largest configuration that fits one B200: p=9, k=3, u=59, 32,768 coarse
+patches (52.2 GB pool), 196,608 faces, order3 interpolation + restriction of
+every face, fine patches read from the pool by index lists; under torchrun
+the patches are block-partitioned over the ranks and cross faces exchange
+source boxes / results over NCCL.  --config 1..4 run the other BASELINE
+configs.  Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement.
 """
 
 from __future__ import annotations
@@ -26,6 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fine ghost-cell values/s (interp+restrict, fp64) and % of HBM roofline"
+PEAK_NORTH_STAR = 8000.0  # GB/s, BASELINE.json north_star's roofline denominator
 
 
 def parse():
@@ -33,12 +37,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--straddle", type=float, default=0.0,
+                    help="config 5: fraction of faces with one fine patch drawn from the whole pool (A/B, tests)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink patch / face counts (tuning runs only)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunks", type=int, default=16, help="pipeline chunks of the e2e leg")
-    ap.add_argument("--cpu-sample", type=int, default=256, help="faces in the CPU baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=512, help="faces per pass in the CPU reference arm's sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-same-level", action="store_true", help="skip the same-level halo fill leg")
@@ -147,6 +153,15 @@ def unit_costs(role, scheme, p, k, u, selectors):
 # our arm
 # ---------------------------------------------------------------------------
 
+def ours_config(s, world, wl=None):
+    """Config dict of configs 1-4, shared by both arms."""
+    return {"workload": f"config{s.config}: {s.name}", "p": s.p, "k": s.k, "u": s.u, "coarse_patches": s.n_patches,
+            "faces": s.n_faces, "passes": [f"{r}:{sc}" for r, sc in s.passes],
+            "layout": "coarse pool (p+2k)^3 AoS + per-face fine restriction slabs (world layout)",
+            "l2": "inputs >> 126 MB L2 (no flush needed)",
+            "parallelism": f"weak: {world} independent shard(s)"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -185,16 +200,16 @@ def run_ours(args, rank, world, local_rank):
             with torch.cuda.stream(side):
                 for ps in passes:
                     if ps["role"] == "interpolate":
-                        ps["batch"].launch(ps["src"], ps["out"], stream=side.cuda_stream, check_flag=False)
+                        ps["batch"].launch(ps["src"], ps["out"], stream=side.cuda_stream)
             for ps in passes:
                 if ps["role"] != "interpolate":
-                    ps["batch"].launch(ps["src"], ps["out"], check_flag=False)
+                    ps["batch"].launch(ps["src"], ps["out"])
             stream.wait_stream(side)
             return
         for i, ps in enumerate(passes):
             if evs is not None:
                 evs[i].record(stream)
-            ps["batch"].launch(ps["src"], ps["out"], check_flag=False)
+            ps["batch"].launch(ps["src"], ps["out"])
         if evs is not None:
             evs[-1].record(stream)
 
@@ -244,23 +259,20 @@ def run_ours(args, rank, world, local_rank):
         gbs = ps["bytes"] / (ms / 1e3) / 1e9
         pass_rows.append({"role": ps["role"], "scheme": ps["scheme"], "faces": ps["n"], "ms": round(ms, 4),
                           "alg_bytes": int(ps["bytes"]), "alg_GBps": round(gbs, 1), "frac_hbm": round(gbs / peak, 3),
-                          "fp64_TFLOPs": round(ps["flops"] / (ms / 1e3) / 1e12, 2)})
+                          "frac_8tbs": round(gbs / PEAK_NORTH_STAR, 3),
+                          "csr_equiv_TFLOPs": round(ps["flops"] / (ms / 1e3) / 1e12, 2)})
     dom = max(range(len(passes)), key=lambda i: per_pass_ms[i])
     result = {
         "metric": METRIC, "value": value, "unit": "values/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded field (BASELINE config text) sampled at cell centres + 1e-6 N(0,1), generated in HBM",
-        "config": {"workload": f"config{s.config}: {s.name}", "p": p, "k": k, "u": u, "coarse_patches": s.n_patches,
-                   "faces": s.n_faces, "passes": [f"{r}:{sc}" for r, sc in s.passes],
-                   "layout": "coarse pool (p+2k)^3 AoS + per-face fine restriction slabs (world layout)",
-                   "l2": f"inputs {(wl.pool.numel() + (wl.fine.numel() if wl.fine is not None else 0)) * 8 / 1e9:.1f} GB"
-                         " >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"weak: {world} independent shard(s)",
+        "config": {**ours_config(s, world, wl),
                    **({"overlap": "interpolation passes on a side stream"} if args.overlap else {})},
         "roofline": {"bound": "hbm", "kernel": f"{passes[dom]['role']}:{passes[dom]['scheme']}",
                      "achieved": pass_rows[dom]["alg_GBps"], "peak": peak, "unit": "GB/s",
-                     "frac": round(pass_rows[dom]["alg_GBps"] / peak, 4), "traffic": None,
+                     "frac": round(pass_rows[dom]["alg_GBps"] / peak, 4),
+                     "frac_8tbs": round(pass_rows[dom]["alg_GBps"] / PEAK_NORTH_STAR, 4), "traffic": None,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"},
         "passes": pass_rows,
         "gpu_launches": args.steps * len(passes),
@@ -280,6 +292,7 @@ def run_ours(args, rank, world, local_rank):
     step_bytes = sum(ps["bytes"] for ps in passes)
     result["step_alg_GBps"] = round(step_bytes / (ms_per_step / 1e3) / 1e9, 1)
     result["step_frac_hbm"] = round(step_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4)
+    result["nonfinite_flag"] = any(ps["batch"].nonfinite() for ps in passes)
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, wl, passes, dev, world)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -334,35 +347,163 @@ def same_level_leg(wl, dev, peak, reps=20):
             "frac_hbm": round(gbs / peak, 3), "sample_bit_exact": ok, "launches": reps}
 
 
+# ---------------------------------------------------------------------------
+# config 5 (default): the largest BASELINE configuration that fits one B200
+# ---------------------------------------------------------------------------
+
+def c5_config(spec, world, straddle=0.0):
+    """The config dict of both arms (ours and --impl reference)."""
+    return {"workload": f"config5: {spec.name}", "p": spec.p, "k": spec.k, "u": spec.u,
+            "coarse_patches": spec.n_patches, "faces": spec.n_faces,
+            "passes": ["interpolate:order3", "restrict:order3"],
+            "fine_sources": "the nine fine patches of every face read from the patch pool by index lists",
+            "cross_faces": "10% of faces: fine patches on a partner rank (uniform); at N=1 all faces are local",
+            **({"straddle": straddle} if straddle else {}),
+            "parallelism": f"{world} rank(s), block-partitioned patches, NCCL P2P for cross faces",
+            "l2": "pool 52.2 GB >> 126 MB L2 (no flush needed)"}
+
+
+def c5_jobs(wl, faces_by_role):
+    """Oracle jobs (exchange, source, output) for {role: face ids}; patches regenerated."""
+    import workloads as W
+    from oracle import exchange as OE
+    from oracle import geometry as OG
+
+    s = wl.spec
+    need = set()
+    for role, ids in faces_by_role.items():
+        for f in ids:
+            need.update([int(wl.coarse[f])] if role == "interpolate" else [int(x) for x in wl.fine[f]])
+    need = np.array(sorted(need), dtype=np.int64)
+    vals = W.patch_values(wl, need)
+    patches = {int(g): vals[i] for i, g in enumerate(need)}
+    jobs = []
+    for role, ids in faces_by_role.items():
+        for f in ids:
+            seg = int(wl.segment[f]) if role == "interpolate" else 0
+            cfg = OG.FaceCfg("xyz"[int(wl.normal[f])], ("negative", "positive")[int(wl.side[f])], seg, s.p, s.k, s.u)
+            ex = OE.exchange_for(cfg, "order3", role)
+            jobs.append((role, int(f), ex, W.face_source(wl, f, role, patches), np.empty(ex.n_out)))
+    return jobs
+
+
+def c5_parity(wl, plan, sweep, per, world, n_sample=16):
+    """Oracle check of sampled output slots on EVERY rank: local faces, faces computed from
+    received source boxes (staged) and faces whose results arrived from a peer; the worst
+    error is reduced to rank 0."""
+    import torch
+
+    from oracle import exchange as OE
+
+    rng = np.random.default_rng(5 + plan.rank)
+    pick = {}
+    counts = {"local": 0, "staged": 0, "received": 0}
+    for role, rp in plan.items():
+        groups = [("local", 0, rp.local.size), ("staged", rp.local.size, rp.local.size + rp.staged.size),
+                  ("received", rp.local.size + rp.staged.size, rp.n_out)]
+        for name, a, b in groups:
+            if b > a:
+                j = rng.choice(np.arange(a, b), min(n_sample, b - a), replace=False)
+                pick.setdefault(role, []).extend(j.tolist())
+                counts[name] += j.size
+    order = {role: rp.out_order() for role, rp in plan.items()}
+    jobs = c5_jobs(wl, {role: [order[role][j] for j in js] for role, js in pick.items()})
+    st = OE.run_many([j[2] for j in jobs], [j[3] for j in jobs], [j[4] for j in jobs], cpu_threads())
+    assert (st == 0).all()
+    worst = 0.0
+    it = iter(jobs)
+    for role, js in pick.items():
+        for j in js:
+            _, _, _, _, want = next(it)
+            got = sweep.out[role][j * per:(j + 1) * per].cpu().numpy()
+            worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))
+    n = sum(counts.values())
+    if world > 1:
+        t = torch.tensor([worst, -float(n)] + [-float(counts[c]) for c in counts], dtype=torch.float64,
+                         device=sweep.out["interpolate"].device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)  # max of worst; -max(-n) = min
+        t2 = torch.tensor([float(n)] + [float(counts[c]) for c in counts], dtype=torch.float64, device=t.device)
+        torch.distributed.all_reduce(t2)
+        worst = float(t[0])
+        n = int(t2[0])
+        counts = {c: int(v) for c, v in zip(counts, t2[1:].tolist())}
+    return {"sample_faces": n, "by_kind": counts, "ranks": world, "max_rel_err": worst, "tol": 1e-12,
+            "ok": worst <= 1e-12}
+
+
+def c5_cpu_baseline(wl, n_per_role=128, budget_s=12.0):
+    """Oracle C port (reference HaloExchange.run restated) on the host cores over a sample of
+    config-5 faces, repeated to fill ~budget_s of CPU time."""
+    from oracle import exchange as OE
+
+    rng = np.random.default_rng(12345)
+    nf = wl.spec.n_faces
+    ids = {r: np.sort(rng.choice(nf, n_per_role, replace=False)) for r in ("interpolate", "restrict")}
+    jobs = c5_jobs(wl, ids)
+    nth = cpu_threads()
+    exs, srcs, outs = [j[2] for j in jobs], [j[3] for j in jobs], [j[4] for j in jobs]
+    OE.run_many(exs, srcs, outs, nth)  # warm
+    reps, t_all = 0, 0.0
+    while t_all < budget_s and reps < 1000:
+        t = time.perf_counter()
+        st = OE.run_many(exs, srcs, outs, nth)
+        t_all += time.perf_counter() - t
+        reps += 1
+    assert (st == 0).all()
+    values = reps * sum(o.size for o in outs)
+    return {"value": values / t_all, "unit": "values/s", "cores": nth, "kind": "port",
+            "sample": f"{n_per_role} interpolation + {n_per_role} restriction faces of config 5 (order3), "
+                      f"x {reps} repetitions = {t_all:.1f} s; oracle C restatement of HaloExchange.run "
+                      f"(reference schemes.py:185-202) over {nth} OpenMP threads"}
+
+
+def alg_bytes_c5(p, k, u, segments_i, n_restrict):
+    """Algorithmic bytes (distinct support cells + output) of the faces of a launch."""
+    b_i, f_i, _ = unit_costs("interpolate", "order3", p, k, u, list(range(9)))
+    per_seg_i = {}
+    from paper_2504_15814_b200.operators import HostOperator
+
+    h = HostOperator("interpolate", "order3", p, k)
+    for sgm in range(9):
+        c = h.csr(segment=sgm)
+        per_seg_i[sgm] = ((np.unique(c.col_indices).size + c.n_rows) * u * 8.0, 2.0 * c.nnz * u)
+    b_r, f_r, _ = unit_costs("restrict", "order3", p, k, u, [None])
+    bi = sum(per_seg_i[int(x)][0] for x in segments_i)
+    fi = sum(per_seg_i[int(x)][1] for x in segments_i)
+    return bi, fi, b_r * n_restrict, f_r * n_restrict
+
+
 def run_multi(args, rank, world, local_rank):
     """Config 5: 32,768 coarse patches block-partitioned over the ranks, 196,608 faces,
     order3 interpolation + restriction of every face, fine patches drawn from the pool
-    by index lists, 10% of faces with their fine patches on another rank (results of
-    those cross NVLink in one grouped NCCL send/recv step, overlapped with local faces).
-    Strong scaling: the job is fixed, ranks split it."""
+    by index lists; 10% of faces have their fine patches on another rank (their source
+    boxes or results cross NVLink in one grouped NCCL send/recv step, overlapped with
+    local faces).  Strong scaling: the job is fixed, ranks split it."""
     import torch
 
     import paper_2504_15814_b200 as th
     import workloads as W
-    from paper_2504_15814_b200.multigpu import GpuCompute, Sweep, plan_sweep
+    from paper_2504_15814_b200.multigpu import NcclTransport, Support, make_rank_sweep, plan_sweep
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    wl = W.build_multi(world, rank, scale=args.scale)
+    t_setup = time.perf_counter()
+    wl = W.describe_multi(world, scale=args.scale, straddle=args.straddle)
     s = wl.spec
     p, k, u = s.p, s.k, s.u
-    plans = plan_sweep(wl.part, wl.coarse, wl.fine, wl.segment, rank)
-    per = k * p * p * u
+    ops = {role: th.operators.DEFAULT_CACHE.device_operator(role, "order3", p, k)
+           for role in ("interpolate", "restrict")}
+    support = Support.from_operators(ops["interpolate"], ops["restrict"], p, k)
+    plan = plan_sweep(wl.part, wl.coarse, wl.fine, wl.segment, rank, wl.normal, wl.side, support=support)
+    wl = W.build_multi(world, rank, scale=args.scale, src_elems=plan.src_elems(p, k, u), straddle=args.straddle)
     lo = int(wl.part.bounds[rank])
-    ops = {role: th.operators.DEFAULT_CACHE.device_operator(role, "order3", p, k) for role in plans}
-
-    def make_records(role, ids):
-        if role == "interpolate":
-            return th.pool_interp_faces(p, k, u, wl.coarse[ids] - lo, wl.normal[ids], wl.side[ids], wl.segment[ids])
-        return th.pool_restrict_faces(p, k, u, wl.fine[ids] - lo, wl.normal[ids], wl.side[ids])
-
-    comp = GpuCompute(plans, make_records, ops, {"interpolate": wl.pool, "restrict": wl.pool}, u)
-    sweep = Sweep(plans, per, dev, torch.float64)
+    per = k * p * p * u
+    if world > 1:
+        torch.distributed.barrier()  # every rank is set up before the first P2P
+    transport = NcclTransport(dev)
+    sweep, comp = make_rank_sweep(plan, ops, support, p, k, u, wl.src, transport, wl.coarse, wl.fine, wl.normal,
+                                  wl.side, wl.segment, lo)
+    t_setup = time.perf_counter() - t_setup
     for _ in range(max(3, args.warmup)):
         sweep.run(comp)
     torch.cuda.synchronize()
@@ -372,97 +513,215 @@ def run_multi(args, rank, world, local_rank):
     sampler.start()
     time.sleep(0.05)
     stream = torch.cuda.current_stream()
+    keys = list(comp.batches)
+    ev_steps = [{kk: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for kk in keys}
+                for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     sampler.mark()
     t0.record(stream)
-    for _ in range(args.steps):
+    for kk in range(args.steps):
+        comp.events = ev_steps[kk]
         sweep.run(comp)
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     clocks = sampler.stop()
+    comp.events = None
+    nonfinite = comp.nonfinite()
     ms = t0.elapsed_time(t1) / args.steps
+    launch_ms = {kk: statistics.mean(ev[kk][0].elapsed_time(ev[kk][1]) for ev in ev_steps) for kk in keys}
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    n_faces = s.n_faces
-    values = 2 * n_faces * per
-    b_i, f_i, _ = unit_costs("interpolate", "order3", p, k, u, list(range(9)))
-    b_r, f_r, _ = unit_costs("restrict", "order3", p, k, u, [None])
-    step_bytes = n_faces * (b_i + b_r) / world
+    values = 2 * s.n_faces * per
     peak, peak_kind = peaks()
-    cross = {r: int(sum(x.size for x in pl.send)) for r, pl in plans.items()}
+    rows = []
+    from paper_2504_15814_b200.multigpu import batch_ids
+
+    for (role, kind) in keys:
+        ids = batch_ids(plan, role, kind)
+        if role == "interpolate":
+            byts, flops, _, _ = alg_bytes_c5(p, k, u, wl.segment[ids], 0)
+        else:
+            _, _, byts, flops = alg_bytes_c5(p, k, u, [], ids.size)
+        byts += ops[role].info.device_bytes
+        m_ = launch_ms[(role, kind)]
+        gbs = byts / (m_ / 1e3) / 1e9
+        rows.append({"role": role, "kind": kind, "faces": int(ids.size), "ms": round(m_, 4), "alg_bytes": int(byts),
+                     "alg_GBps": round(gbs, 1), "frac_hbm": round(gbs / peak, 4),
+                     "frac_8tbs": round(gbs / PEAK_NORTH_STAR, 4),
+                     "csr_equiv_TFLOPs": round(flops / (m_ / 1e3) / 1e12, 2)})
+    dom = max(range(len(rows)), key=lambda i: rows[i]["ms"])
+    step_bytes = sum(r["alg_bytes"] for r in rows)
     res = {
         "metric": METRIC, "value": values / (ms / 1e3), "unit": "values/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic cubic field + 1e-6 noise in HBM; fine patches drawn from the pool by index lists",
-        "config": {"workload": f"config5: {s.name}", "p": p, "k": k, "u": u, "coarse_patches": s.n_patches,
-                   "faces": n_faces, "passes": ["interpolate:order3", "restrict:order3"],
-                   "parallelism": f"{world} ranks, block-partitioned patches, NCCL P2P for cross faces",
-                   "cross_faces_sent_rank0": cross},
-        "roofline": {"bound": "hbm", "kernel": "interpolate+restrict:order3 (whole sweep, per rank)",
-                     "achieved": round(step_bytes / (ms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(step_bytes / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
-                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"},
-        "gpu_launches": args.steps * comp.launches,
+        "data": "synthetic: cubic polynomial field per unknown + 1e-6 N(0,1) noise, generated in HBM (seeded per "
+                "64-patch group, partition-independent); fine patches drawn from the pool by index lists",
+        "config": c5_config(s, world, args.straddle),
+        "roofline": {"bound": "hbm", "kernel": f"{rows[dom]['role']}:order3 ({rows[dom]['kind']} faces)",
+                     "achieved": rows[dom]["alg_GBps"], "peak": peak, "unit": "GB/s", "frac": rows[dom]["frac_hbm"],
+                     "frac_8tbs": rows[dom]["frac_8tbs"], "traffic": None,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy); frac_8tbs against the "
+                                  f"north star's 8 TB/s"},
+        "passes": rows,
+        "step_alg_GBps": round(step_bytes / (ms / 1e3) / 1e9, 1),
+        "step_frac_hbm": round(step_bytes / (ms / 1e3) / 1e9 / peak, 4),
+        "step_frac_8tbs": round(step_bytes / (ms / 1e3) / 1e9 / PEAK_NORTH_STAR, 4),
+        "exchange": {"src_boxes_sent": int(sum(b.size for b in plan.src_send)),
+                     "src_bytes_sent": int(plan.n_src_send_cells * u * 8),
+                     "results_sent": {r: rp.n_send for r, rp in plan.items()},
+                     "staged_faces": {r: int(rp.staged.size) for r, rp in plan.items()},
+                     "rank": rank},
+        "gpu_launches": args.steps * (comp.launches + (1 if sweep.pack is not None else 0)
+                                      + (1 if sweep.unpack is not None else 0)),
+        "nonfinite_flag": nonfinite,
         "clocks": clocks,
+        "setup_s": round(t_setup, 1),
     }
-    if rank == 0 and not args.no_cpu:
-        res["parity"] = multi_parity(wl, plans, sweep, per)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get("config5", {})
+        ent = tr.get(f"{rows[dom]['role']}:order3")
+        if isinstance(ent, dict):
+            res["roofline"]["traffic"] = round(ent["bytes"] * rows[dom]["faces"] / ent["faces"])
+            res["roofline"]["traffic_source"] = ("profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum "
+                                                 f"of one ncu --set full launch over {ent['faces']} faces, per face)")
+    except (OSError, ValueError):
+        pass
+    if not args.no_e2e:
+        res["e2e"] = run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world)
+    res["parity"] = c5_parity(wl, plan, sweep, per, world)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = c5_cpu_baseline(wl)
     return res
 
 
-def multi_parity(wl, plans, sweep, per, n_sample=24):
-    """Oracle check of a sample of faces computed and kept on this rank."""
-    from oracle import exchange as OE
-    from oracle import geometry as OG
+def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world, n_chunks=16):
+    """Config 5 end to end through the C ABI with HOST buffers: every step ships this rank's
+    patch pool from registered (page-locked) host memory into HBM (th_memcpy_async, 16 chunks),
+    runs the sweep through th_apply_faces — interpolation of the local faces starts chunk by
+    chunk as their coarse patches arrive, restriction (nine random fine patches per face) after
+    the whole pool — and reads every result back into registered host memory
+    (th_memcpy_async), overlapping the pool upload."""
+    import torch
 
-    s = wl.spec
-    p, k, u = s.p, s.k, s.u
+    import paper_2504_15814_b200 as th
+    from paper_2504_15814_b200 import _native
+
+    lib = _native.load()
+    pool = wl.pool
+    n_pool = pool.numel()
+    host_pool = np.empty(n_pool, dtype=np.float64)
+    outs = {r: sweep.out[r][: rp.n_out * k * p * p * u] for r, rp in plan.items()}
+    host_out = {r: np.empty(t.numel(), dtype=np.float64) for r, t in outs.items()}
+    reg = torch._C._cudart
+    registered = []
+    for a in [host_pool] + list(host_out.values()):
+        if a.size:
+            rc = reg.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister failed: {rc}")
+            registered.append(a)
+    # host copy of the pool (setup, not timed)
+    step_c = 1 << 27
+    for a in range(0, n_pool, step_c):
+        b = min(n_pool, a + step_c)
+        _native.check(lib.th_memcpy_async(host_pool.ctypes.data + a * 8, pool[a:b].data_ptr(), (b - a) * 8, 1,
+                                          torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
     E = p + 2 * k
-    lo = int(wl.part.bounds[0])
-    pool = wl.pool.view(-1, E, E, E, u)
-    rng = np.random.default_rng(5)
-    worst = 0.0
-    for role, plan in plans.items():
-        pick = rng.choice(plan.local.size, min(n_sample, plan.local.size), replace=False)
-        for j in pick:
-            f = int(plan.local[j])
-            n, sd = int(wl.normal[f]), int(wl.side[f])
-            t1, t2 = [d for d in range(3) if d != n]
-            if role == "interpolate":
-                lo3, ext = [k, k, k], [p, p, p]
-                lo3[n], ext[n] = (p if sd == 0 else 0), 2 * k
-                c = int(wl.coarse[f]) - lo
-                src = pool[c, lo3[2]:lo3[2] + ext[2], lo3[1]:lo3[1] + ext[1], lo3[0]:lo3[0] + ext[0]].cpu().numpy().reshape(-1)
-                seg = int(wl.segment[f])
-            else:
-                ext = [3 * p, 3 * p, 3 * p]
-                ext[n] = 2 * k
-                world_box = np.zeros((ext[2], ext[1], ext[0], u))
-                for b in range(9):
-                    lo3, e = [k, k, k], [p, p, p]
-                    lo3[n], e[n] = (0 if sd == 0 else p), 2 * k
-                    blk = pool[int(wl.fine[f, b]) - lo, lo3[2]:lo3[2] + e[2], lo3[1]:lo3[1] + e[1],
-                               lo3[0]:lo3[0] + e[0]].cpu().numpy()
-                    off = [0, 0, 0]
-                    off[t1], off[t2] = (b % 3) * p, (b // 3) * p
-                    world_box[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = blk
-                src = world_box.reshape(-1)
-                seg = 0
-            cfg = OG.FaceCfg("xyz"[n], ("negative", "positive")[sd], seg, p, k, u)
-            ex = OE.exchange_for(cfg, "order3", role)
-            want = np.empty(ex.n_out)
-            ex.run(src, want)
-            got = sweep.out[role][j * per:(j + 1) * per].cpu().numpy()
-            worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))
-    return {"sample_faces": 2 * n_sample, "max_rel_err": worst, "tol": 1e-12, "ok": worst <= 1e-12}
+    patch = E ** 3 * u
+    n_local = plan.n_local
+    rp_i = plan["interpolate"]
+    # local interpolation faces are in coarse-patch order: chunk c's faces are a contiguous range
+    cb = [(n_local * c) // n_chunks for c in range(n_chunks + 1)]
+    loc = wl.coarse[rp_i.local] - lo
+    cut = np.searchsorted(loc, cb)
+    per = k * p * p * u
+    chunk_batches = []
+    for c in range(n_chunks):
+        a, b = int(cut[c]), int(cut[c + 1])
+        ids = rp_i.local[a:b]
+        if b > a:
+            rec = th.pool_interp_faces(p, k, u, wl.coarse[ids] - lo, wl.normal[ids], wl.side[ids], wl.segment[ids],
+                                       dst_offsets=np.arange(a, b, dtype=np.int64) * per)
+            chunk_batches.append((th.FaceBatch(ops["interpolate"], rec, u), a, b))
+        else:
+            chunk_batches.append((None, a, b))
+    s_in, s_run, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    n_i_out = rp_i.n_out
+
+    def d2h(role, a, b):
+        _native.check(lib.th_memcpy_async(host_out[role].ctypes.data + a * per * 8, outs[role][a * per:].data_ptr(),
+                                          (b - a) * per * 8, 1, s_out.cuda_stream))
+
+    def e2e_step():
+        evs = []
+        for c in range(n_chunks):
+            a, b = cb[c] * patch, cb[c + 1] * patch
+            _native.check(lib.th_memcpy_async(pool[a:].data_ptr(), host_pool.ctypes.data + a * 8, (b - a) * 8, 0,
+                                              s_in.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+            evs.append(ev)
+        with torch.cuda.stream(s_run):
+            for c, (batch, a, b) in enumerate(chunk_batches):
+                s_run.wait_event(evs[c])
+                if batch is not None:
+                    batch.launch(wl.src, sweep.out["interpolate"], stream=s_run.cuda_stream)
+                    e = torch.cuda.Event()
+                    e.record(s_run)
+                    s_out.wait_event(e)
+                    d2h("interpolate", a, b)
+            sweep.pre(comp)
+            sweep.local(comp, roles=("restrict",))
+            sweep.post(comp)
+            e = torch.cuda.Event()
+            e.record(s_run)
+        s_out.wait_event(e)
+        if n_i_out > rp_i.local.size:
+            d2h("interpolate", rp_i.local.size, n_i_out)
+        n_r = plan["restrict"].n_out
+        for c in range(4):
+            d2h("restrict", n_r * c // 4, n_r * (c + 1) // 4)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(max(1, args.e2e_steps)):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        e2e_step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t)
+    t_step = statistics.median(times)
+    if world > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    # host results equal the device-resident sweep's (same pool, same faces)
+    agree = all(np.array_equal(host_out[r][:per * 64], outs[r][:per * 64].cpu().numpy()) for r in outs)
+    for a in registered:
+        reg.cudaHostUnregister(a.ctypes.data)
+    values = 2 * wl.spec.n_faces * per
+    return {"value": values / t_step, "unit": "values/s",
+            "h2d_bytes_per_step": int(n_pool * 8),
+            "d2h_bytes_per_step": int(sum(t.numel() for t in outs.values()) * 8),
+            "ms_per_step": round(t_step * 1e3, 1), "steps": len(times), "matches_device_run": agree,
+            "how": "per step: the rank's patch pool (host memory page-locked with cudaHostRegister) -> HBM in 16 "
+                   "chunks (th_memcpy_async); order3 interpolation of the local faces chunk by chunk as their "
+                   "coarse patches land, then the sweep (th_copy_boxes packing, NCCL P2P, restriction) through "
+                   "th_apply_faces; every result -> page-locked host memory (th_memcpy_async), the interpolation "
+                   "results overlapping the upload; wall clock with device sync, max over ranks"}
 
 
 def run_e2e(args, wl, passes, dev, world):
@@ -561,7 +820,7 @@ def run_e2e(args, wl, passes, dev, world):
             with torch.cuda.stream(s_run):
                 for ps, od, (batch, lo_, hi_) in zip(passes, outs_d, ch["batches"]):
                     if batch is not None:
-                        batch.launch(d_i if ps["role"] == "interpolate" else d_r, od, check_flag=False)
+                        batch.launch(d_i if ps["role"] == "interpolate" else d_r, od)
                 e_run = torch.cuda.Event()
                 e_run.record(s_run)
             s_out.wait_event(e_run)
@@ -673,27 +932,76 @@ def cpu_baseline(args, wl, passes):
 # and cannot travel to the GPU box) on the host cores, same config and metric
 # ---------------------------------------------------------------------------
 
+def c5_host_source(wl, f, role, rng):
+    """Host (numpy) world-layout source buffer of config-5 face f for one role: the field at
+    the pool cells it reads (coarse patch box, or the nine fine patches' blocks) + fresh noise.
+    The CPU reference arm builds its inputs with this (it must not need a GPU)."""
+    s = wl.spec
+    p, k, u, m, H = s.p, s.k, s.u, wl.m, wl.H
+    n, sd = int(wl.normal[f]), int(wl.side[f])
+    t1, t2 = [d for d in range(3) if d != n]
+
+    def block(pid, lo3, ext):
+        pos = np.array([pid % m, (pid // m) % m, pid // (m * m)], dtype=np.float64)
+        ax = [np.arange(lo3[d], lo3[d] + ext[d]) - k + 0.5 for d in range(3)]
+        zz, yy, xx = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+        xyz = (pos * p + np.stack([xx.ravel(), yy.ravel(), zz.ravel()], axis=1)) * H
+        v = wl.fld.eval_numpy(xyz) + 1e-6 * rng.standard_normal((xyz.shape[0], u))
+        return v.reshape(ext[2], ext[1], ext[0], u)
+
+    if role == "interpolate":
+        lo3, ext = [k, k, k], [p, p, p]
+        lo3[n], ext[n] = (p if sd == 0 else 0), 2 * k
+        return np.ascontiguousarray(block(int(wl.coarse[f]), lo3, ext).reshape(-1))
+    ext = [3 * p, 3 * p, 3 * p]
+    ext[n] = 2 * k
+    box = np.zeros((ext[2], ext[1], ext[0], u))
+    for b in range(9):
+        lo3, e = [k, k, k], [p, p, p]
+        lo3[n], e[n] = (0 if sd == 0 else p), 2 * k
+        off = [0, 0, 0]
+        off[t1], off[t2] = (b % 3) * p, (b // 3) * p
+        box[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = block(int(wl.fine[f, b]), lo3, e)
+    return box.reshape(-1)
+
+
 def run_reference(args):
     import workloads as W
     from oracle import exchange as OE
     from oracle import geometry as OG
 
-    wl = W.describe(args.config)
-    s = wl.spec
-    p, k, u = s.p, s.k, s.u
     rng = np.random.default_rng(777)
     nth = cpu_threads()
-    n_sample = min(args.cpu_sample, s.n_faces)
-    fc = wl.faces
     jobs = []
-    for role, scheme in s.passes:
-        ids = wl.interp_ids if role == "interpolate" else wl.restrict_ids
-        pick = np.sort(rng.choice(ids, min(n_sample, ids.size), replace=False))
-        for f in pick:
-            seg = int(fc.segment[f]) if role == "interpolate" else 0
-            cfg = OG.FaceCfg("xyz"[fc.normal[f]], ("negative", "positive")[fc.side[f]], seg, p, k, u)
-            ex = OE.exchange_for(cfg, scheme, role)
-            jobs.append((ex, W.host_sources(wl, int(f), role, rng), np.empty(ex.n_out)))
+    if args.config == 5:
+        wl = W.describe_multi(args.gpus, scale=args.scale, straddle=args.straddle)
+        s = wl.spec
+        p, k, u = s.p, s.k, s.u
+        n_sample = min(args.cpu_sample, s.n_faces)
+        for role in ("interpolate", "restrict"):
+            for f in np.sort(rng.choice(s.n_faces, n_sample, replace=False)):
+                seg = int(wl.segment[f]) if role == "interpolate" else 0
+                cfg = OG.FaceCfg("xyz"[int(wl.normal[f])], ("negative", "positive")[int(wl.side[f])], seg, p, k, u)
+                ex = OE.exchange_for(cfg, "order3", role)
+                jobs.append((ex, c5_host_source(wl, f, role, rng), np.empty(ex.n_out)))
+        config = c5_config(s, args.gpus, args.straddle)
+        passes = ("interpolate:order3", "restrict:order3")
+    else:
+        wl = W.describe(args.config)
+        s = wl.spec
+        p, k, u = s.p, s.k, s.u
+        n_sample = min(args.cpu_sample, s.n_faces)
+        fc = wl.faces
+        for role, scheme in s.passes:
+            ids = wl.interp_ids if role == "interpolate" else wl.restrict_ids
+            pick = np.sort(rng.choice(ids, min(n_sample, ids.size), replace=False))
+            for f in pick:
+                seg = int(fc.segment[f]) if role == "interpolate" else 0
+                cfg = OG.FaceCfg("xyz"[fc.normal[f]], ("negative", "positive")[fc.side[f]], seg, p, k, u)
+                ex = OE.exchange_for(cfg, scheme, role)
+                jobs.append((ex, W.host_sources(wl, int(f), role, rng), np.empty(ex.n_out)))
+        config = ours_config(s, args.gpus, wl)
+        passes = tuple(f"{r}:{sc}" for r, sc in s.passes)
     exs, srcs, outs = zip(*jobs)
 
     def step():
@@ -708,13 +1016,13 @@ def run_reference(args):
     dt = (time.perf_counter() - t) / args.steps
     values = sum(o.size for o in outs)
     value = values / dt
-    sample = (f"{len(jobs)} face-passes per step ({n_sample} faces per pass) drawn from config{s.config}; "
-              f"oracle C restatement of HaloExchange.run (reference schemes.py:185-202) over {nth} OpenMP threads")
+    sample = (f"{len(jobs)} face-passes per step ({n_sample} faces per pass: {', '.join(passes)}) drawn from "
+              f"config{s.config}; oracle C restatement of HaloExchange.run (reference schemes.py:185-202) over "
+              f"{nth} OpenMP threads; values/s of the sample = the job's rate (faces are independent)")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "values/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator, host numpy)",
-            "config": {"workload": f"config{s.config}: {s.name}", "p": p, "k": k, "u": u,
-                       "passes": [f"{r}:{sc}" for r, sc in s.passes]},
+            "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same field and face generators, host numpy)", "config": config,
             "cpu_baseline": {"value": value, "unit": "values/s", "cores": nth, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "values/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 

@@ -22,6 +22,12 @@
  *   th_scheme_feasible       scheme_feasible (schemes.py:23-47).
  *   th_copy_faces            same-level halo fill between patches of one level
  *                            (outside the reference).
+ *   th_copy_boxes            strided cell-box copies: packing / unpacking the
+ *                            source boxes of faces whose coarse and fine patches
+ *                            live on different GPUs (outside the
+ *                            reference, which is single-process).
+ *   th_operator_source_box   the source cells an operator's kernels read for
+ *                            one segment / half (the box a cross face ships).
  *
  * Conventions
  *   - Cell data are AoS: the u unknowns of a cell are contiguous (stride 1),
@@ -97,6 +103,18 @@ typedef struct th_face {
   int32_t half;    /* restriction only: TH_HALF_* */
 } th_face;
 
+/* One cell box for th_copy_boxes: ext[0] x ext[1] x ext[2] cells (world x, y, z)
+ * at element offset src (strides src_stride, per world axis) copied to element
+ * offset dst (strides dst_stride); u unknowns per cell, unknown stride 1. */
+typedef struct th_box {
+  int64_t src;
+  int64_t dst;
+  int64_t src_stride[3];
+  int64_t dst_stride[3];
+  int32_t ext[3];
+  int32_t pad;
+} th_box;
+
 typedef struct th_operator th_operator;
 
 typedef struct th_operator_info {
@@ -171,6 +189,25 @@ int32_t th_copy_box_layers(const double* src, double* dst, int64_t n_faces, int3
  * the boxes do not overlap.  All pointers device. */
 int32_t th_copy_faces(const double* src, double* dst, const th_face* faces, int64_t n_faces, int32_t n_ext,
                       int32_t t_ext, int32_t u, void* stream);
+
+/* Asynchronous byte copy on `stream`: kind 0 host->device, 1 device->host, 2 device->device
+ * (host memory pinned or registered).  Moves patch pools and results between host buffers and
+ * HBM for callers that hold their data on the host. */
+int32_t th_memcpy_async(void* dst, const void* src, int64_t bytes, int32_t kind, void* stream);
+
+/* Copy n_boxes cell boxes (th_box records in DEVICE memory) from src to dst, both
+ * device.  Boxes must not overlap one another's targets, nor a target overlap a
+ * source of the same launch.  Bit-exact. */
+int32_t th_copy_boxes(const double* src, double* dst, const th_box* boxes, int64_t n_boxes, int32_t u,
+                      void* stream);
+
+/* Union of the source windows the kernels read for one face selection, in
+ * reference source coordinates: box = {lo0, count0, lo1, count1, lo2, count2}
+ * along (normal, t1, t2) of the reference source region (interpolation: 2k x p x p,
+ * selector = segment 0..8; restriction: 2k x 3p x 3p, selector = TH_HALF_*).
+ * Every source cell outside the box is never read, so a face whose source
+ * arrives from another GPU needs only this box. */
+int32_t th_operator_source_box(const th_operator* op, int32_t selector, int32_t* box);
 
 /* CSR apply on reference-frame AoS buffers (csr.py:143-173); all pointers device. */
 int32_t th_csr_apply(const int64_t* row_offsets, const int64_t* col_indices, const double* values,

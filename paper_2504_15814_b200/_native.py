@@ -44,6 +44,17 @@ FACE_DTYPE = np.dtype([
 ])
 assert FACE_DTYPE.itemsize == 144
 
+# numpy mirror of struct th_box (80 bytes)
+BOX_DTYPE = np.dtype([
+    ("src", "<i8"),
+    ("dst", "<i8"),
+    ("src_stride", "<i8", (3,)),
+    ("dst_stride", "<i8", (3,)),
+    ("ext", "<i4", (3,)),
+    ("pad", "<i4"),
+])
+assert BOX_DTYPE.itemsize == 80
+
 
 class OperatorInfo(ctypes.Structure):
     _fields_ = [
@@ -59,6 +70,7 @@ EXPORTED = (
     "th_operator_create_host",
     "th_operator_destroy", "th_operator_info_get", "th_operator_export_rows", "th_apply_faces",
     "th_check_finite", "th_csr_apply", "th_operator_support_layers", "th_copy_box_layers", "th_copy_faces",
+    "th_copy_boxes", "th_operator_source_box", "th_memcpy_async",
 )
 
 _lib = None
@@ -106,6 +118,12 @@ def load():
     lib.th_copy_box_layers.argtypes = [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp]
     lib.th_copy_faces.restype = _i32
     lib.th_copy_faces.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp]
+    lib.th_copy_boxes.restype = _i32
+    lib.th_copy_boxes.argtypes = [_vp, _vp, _vp, _i64, _i32, _vp]
+    lib.th_operator_source_box.restype = _i32
+    lib.th_operator_source_box.argtypes = [_vp, _i32, ctypes.POINTER(_i32)]
+    lib.th_memcpy_async.restype = _i32
+    lib.th_memcpy_async.argtypes = [_vp, _vp, _i64, _i32, _vp]
     lib.th_csr_apply.restype = _i32
     lib.th_csr_apply.argtypes = [_vp, _vp, _vp, _i64, _vp, _vp, _i32, _vp]
     _lib = lib

@@ -1121,6 +1121,98 @@ int32_t th_copy_faces(const double* src, double* dst, const th_face* faces, int6
   return TH_OK;
 }
 
+// Strided box copy (multi-GPU packing / unpacking of cross-face source boxes): box b moves
+// ext[0] x ext[1] x ext[2] cells (world x, y, z) of u unknowns from src + boxes[b].src to
+// dst + boxes[b].dst, each side addressed through its own world strides.  Warp per (box,
+// eighth of its values); when both sides keep the cells of an x-run contiguous (x stride == u)
+// the run is copied as ext[0] * u consecutive doubles.
+__global__ void __launch_bounds__(256) strided_box_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                          const th_box* __restrict__ boxes, int64_t n_boxes, int u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t units = n_boxes * kCopyChunks;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < units; w += nw) {
+    const th_box* bp = boxes + w / kCopyChunks;
+    const int c = int(w % kCopyChunks);
+    const int ex = __ldg(&bp->ext[0]), ey = __ldg(&bp->ext[1]), ez = __ldg(&bp->ext[2]);
+    const int64_t s0 = __ldg(&bp->src), d0 = __ldg(&bp->dst);
+    const int64_t sx = __ldg(&bp->src_stride[0]), sy = __ldg(&bp->src_stride[1]), sz = __ldg(&bp->src_stride[2]);
+    const int64_t dx = __ldg(&bp->dst_stride[0]), dy = __ldg(&bp->dst_stride[1]), dz = __ldg(&bp->dst_stride[2]);
+    const int64_t n = int64_t(ex) * u;  // values per x-run
+    const int64_t total = n * ey * ez;
+    const int64_t beg = total * c / kCopyChunks, end = total * (c + 1) / kCopyChunks;
+    const bool runs = sx == u && dx == u;
+    for (int64_t e = beg + lane; e < end; e += 32) {
+      const int64_t r = e / n;
+      const int64_t j = e - r * n;
+      const int y = int(r % ey), z = int(r / ey);
+      int64_t so = s0 + y * sy + z * sz, dof = d0 + y * dy + z * dz;
+      if (runs) {
+        so += j;
+        dof += j;
+      } else {
+        const int64_t cell = j / u, q = j - cell * u;
+        so += cell * sx + q;
+        dof += cell * dx + q;
+      }
+      dst[dof] = __ldg(src + so);
+    }
+  }
+}
+
+int32_t th_copy_boxes(const double* src, double* dst, const th_box* boxes, int64_t n_boxes, int32_t u, void* stream) {
+  if (n_boxes < 0) return fail(TH_ERR_CONFIG, "n_boxes must be >= 0");
+  if (n_boxes == 0) return TH_OK;
+  if (!src || !dst || !boxes) return fail(TH_ERR_CONTRACT, "NULL source, target or box pointer");
+  if (u < 1) return fail(TH_ERR_CONFIG, "u must be >= 1");
+  const int64_t units = n_boxes * kCopyChunks;
+  const int blocks = int(std::min<int64_t>((units + 7) / 8, int64_t(num_sms()) * 8));
+  strided_box_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, boxes, n_boxes, u);
+  TH_CUDA(cudaGetLastError());
+  return TH_OK;
+}
+
+int32_t th_operator_source_box(const th_operator* op, int32_t selector, int32_t* box) {
+  if (!op || !box) return fail(TH_ERR_CONFIG, "NULL argument");
+  const th::HostOperator& h = op->host;
+  int g0a, g0b, ga[2], gb[2];
+  if (h.role == 0) {
+    if (selector < 0 || selector > 8) return fail(TH_ERR_CONFIG, "segment must be in [0, 8]");
+    g0a = 0;
+    g0b = int(h.groups[0].size());
+    ga[0] = h.seg_g[selector % 3][0], gb[0] = h.seg_g[selector % 3][1];
+    ga[1] = h.seg_g[selector / 3][0], gb[1] = h.seg_g[selector / 3][1];
+  } else {
+    if (selector < 0 || selector > 2) return fail(TH_ERR_CONFIG, "half must be TH_HALF_FULL, _INNER or _OUTER");
+    g0a = h.half_g[selector][0];
+    g0b = h.half_g[selector][1];
+    ga[0] = ga[1] = 0;
+    gb[0] = gb[1] = int(h.groups[1].size());
+  }
+  auto span = [](const std::vector<th::Group>& g, int a, int b, int32_t* out) {
+    int lo = 1 << 30, hi = -1;
+    for (int i = a; i < b; ++i) {
+      lo = std::min(lo, g[i].win0);
+      hi = std::max(hi, g[i].win0 + g[i].winL);
+    }
+    out[0] = hi > lo ? lo : 0;
+    out[1] = hi > lo ? hi - lo : 0;
+  };
+  span(h.groups[0], g0a, g0b, box);
+  span(h.groups[1], ga[0], gb[0], box + 2);
+  span(h.groups[1], ga[1], gb[1], box + 4);
+  return TH_OK;
+}
+
+int32_t th_memcpy_async(void* dst, const void* src, int64_t bytes, int32_t kind, void* stream) {
+  if (bytes < 0) return fail(TH_ERR_CONFIG, "bytes must be >= 0");
+  if (bytes == 0) return TH_OK;
+  if (!src || !dst) return fail(TH_ERR_CONTRACT, "NULL pointer");
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  TH_CUDA(cudaMemcpyAsync(dst, src, size_t(bytes), k, static_cast<cudaStream_t>(stream)));
+  return TH_OK;
+}
+
 int32_t th_operator_support_layers(const th_operator* op, int32_t* lo, int32_t* count) {
   if (!op || !lo || !count) return fail(TH_ERR_CONFIG, "NULL argument");
   int a = op->host.ax[0].ns, b = 0;

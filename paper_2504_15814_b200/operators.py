@@ -112,6 +112,13 @@ class HostOperator:
         _native.check(_native.load().th_operator_support_layers(self.handle, ctypes.byref(lo), ctypes.byref(cnt)))
         return lo.value, cnt.value
 
+    def source_box(self, selector: int) -> tuple:
+        """(lo0, n0, lo1, n1, lo2, n2): reference source cells the kernels read for a segment
+        (interpolation) or half code (restriction), along (normal, t1, t2)."""
+        box = (ctypes.c_int32 * 6)()
+        _native.check(_native.load().th_operator_source_box(self.handle, int(selector), box))
+        return tuple(int(v) for v in box)
+
     @property
     def max_condition(self) -> float:
         return float(self.info.max_condition)

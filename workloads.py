@@ -343,10 +343,16 @@ class MultiWorkload:
     m: int
     H: float
     pool: object = None       # this rank's patches [lo, hi)
+    src: object = None        # source tensor: pool + staging slots + received boxes
 
 
-def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10) -> MultiWorkload:
-    """Global face list of config 5 (identical on every rank)."""
+def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10, straddle: float = 0.0) -> MultiWorkload:
+    """Global face list of config 5 (identical on every rank).
+
+    BASELINE: 10% of faces have coarse and fine patches on different GPUs, the partner GPU
+    uniform at random; all nine fine patches of such a face live on the partner.  With
+    ``straddle`` > 0 that fraction of faces additionally gets one fine patch drawn from the
+    whole pool (its nine fine patches then straddle GPUs; tests and A/B runs only)."""
     from paper_2504_15814_b200.multigpu import Partition
 
     spec = SPECS[5]
@@ -368,21 +374,106 @@ def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10) -> Multi
     lo = part.bounds[f_own]
     size = part.bounds[f_own + 1] - lo
     fine = lo[:, None] + (rng.random((nf, 9)) * size[:, None]).astype(np.int64)
+    if straddle > 0:
+        srng = np.random.default_rng(spec.seed + 17)
+        st = srng.random(nf) < straddle
+        fine[st, srng.integers(0, 9, int(st.sum()))] = srng.integers(0, n, int(st.sum()))
     m = lattice(n)
     return MultiWorkload(spec, fld, part, coarse.astype(np.int64), (orient // 2).astype(np.int64),
                          (orient % 2).astype(np.int64), segment.astype(np.int64), fine, m, 1.0 / (m * spec.p))
 
 
-def build_multi(world: int, rank: int, scale: float = 1.0) -> MultiWorkload:
+NOISE_GROUP = 64  # patches per noise generator
+
+
+def _patch_group(wl: MultiWorkload, g: int, device):
+    """Values of patches [g*64, g*64 + 64) clipped to the pool: field + 1e-6 N(0,1) noise from a
+    generator seeded with (seed, g), so a patch's values do not depend on the partition."""
     import torch
 
-    wl = describe_multi(world, scale)
+    s = wl.spec
+    per = (s.p + 2 * s.k) ** 3
+    a, b = g * NOISE_GROUP, min((g + 1) * NOISE_GROUP, s.n_patches)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(s.seed * 1000003 + g)
+    noise = 1e-6 * torch.randn((NOISE_GROUP, per, s.u), dtype=torch.float64, device=device, generator=gen)
+    vals = wl.fld.eval_torch(patch_cell_centres(s, wl.m, wl.H, np.arange(a, b))).reshape(b - a, per, s.u)
+    return vals + noise[: b - a]
+
+
+def fill_pool(wl: MultiWorkload, rank: int, pool) -> None:
+    """Fill `pool` with this rank's patches [lo, hi) of the global pool (E^3 u values each)."""
+    s = wl.spec
+    per = (s.p + 2 * s.k) ** 3
+    lo, hi = int(wl.part.bounds[rank]), int(wl.part.bounds[rank + 1])
+    view = pool[: (hi - lo) * per * s.u].view(hi - lo, per, s.u)
+    for g in range(lo // NOISE_GROUP, (hi + NOISE_GROUP - 1) // NOISE_GROUP):
+        vals = _patch_group(wl, g, pool.device)
+        a = g * NOISE_GROUP
+        a0, b0 = max(a, lo), min(a + vals.shape[0], hi)
+        view[a0 - lo:b0 - lo] = vals[a0 - a:b0 - a]
+
+
+def patch_values(wl: MultiWorkload, ids, device="cuda"):
+    """(len(ids), E, E, E, u) values of global patches `ids` (any rank's), regenerated."""
+    import torch
+
+    s = wl.spec
+    E = s.p + 2 * s.k
+    ids = np.asarray(ids, dtype=np.int64)
+    out = torch.empty((ids.size, E, E, E, s.u), dtype=torch.float64, device=device)
+    for g in np.unique(ids // NOISE_GROUP):
+        vals = _patch_group(wl, int(g), device).view(-1, E, E, E, s.u)
+        sel = np.flatnonzero(ids // NOISE_GROUP == g)
+        out[torch.as_tensor(sel, device=device)] = vals[torch.as_tensor(ids[sel] - g * NOISE_GROUP, device=device)]
+    return out
+
+
+def build_multi(world: int, rank: int, scale: float = 1.0, src_elems: int | None = None,
+                straddle: float = 0.0) -> MultiWorkload:
+    """Config 5 on this rank: its pool (patches [lo, hi)) at the front of a source tensor of
+    `src_elems` elements (multigpu.SweepPlan.src_elems: pool + staging + received boxes)."""
+    import torch
+
+    wl = describe_multi(world, scale, straddle=straddle)
     s = wl.spec
     E = s.p + 2 * s.k
     lo, hi = int(wl.part.bounds[rank]), int(wl.part.bounds[rank + 1])
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(s.seed + 7919 * rank)
-    wl.pool = torch.empty(max(1, (hi - lo) * E ** 3 * s.u), dtype=torch.float64, device="cuda")
-    _fill(wl.pool, lambda a, b: patch_cell_centres(s, wl.m, wl.H, np.arange(lo + a, lo + b)), hi - lo, E ** 3,
-          wl.fld, s.u, gen)
+    n_pool = (hi - lo) * E ** 3 * s.u
+    wl.src = torch.empty(max(1, n_pool, src_elems or 0), dtype=torch.float64, device="cuda")
+    wl.src[n_pool:].zero_()
+    wl.pool = wl.src[:n_pool]
+    fill_pool(wl, rank, wl.pool)
     return wl
+
+
+def face_source(wl: MultiWorkload, f: int, role: str, patches) -> np.ndarray:
+    """World-layout reference source buffer (numpy) of config-5 face f, cut from patch arrays
+    {global id: (E, E, E, u)} (torch or numpy): the buffer the reference HaloExchange.run takes
+    (interpolation: the coarse patch's 2k x p x p box; restriction: the nine fine patches'
+    2k x p x p blocks side by side, geometry.py:244-261)."""
+    s = wl.spec
+    p, k, u = s.p, s.k, s.u
+    n, sd = int(wl.normal[f]), int(wl.side[f])
+    t1, t2 = [d for d in range(3) if d != n]
+
+    def host(x):
+        return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+    if role == "interpolate":
+        lo3, ext = [k, k, k], [p, p, p]
+        lo3[n], ext[n] = (p if sd == 0 else 0), 2 * k
+        v = patches[int(wl.coarse[f])]
+        return np.ascontiguousarray(host(v[lo3[2]:lo3[2] + ext[2], lo3[1]:lo3[1] + ext[1],
+                                           lo3[0]:lo3[0] + ext[0]]).reshape(-1))
+    ext = [3 * p, 3 * p, 3 * p]
+    ext[n] = 2 * k
+    box = np.zeros((ext[2], ext[1], ext[0], u))
+    for b in range(9):
+        lo3, e = [k, k, k], [p, p, p]
+        lo3[n], e[n] = (0 if sd == 0 else p), 2 * k
+        blk = patches[int(wl.fine[f, b])][lo3[2]:lo3[2] + e[2], lo3[1]:lo3[1] + e[1], lo3[0]:lo3[0] + e[0]]
+        off = [0, 0, 0]
+        off[t1], off[t2] = (b % 3) * p, (b // 3) * p
+        box[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = host(blk)
+    return box.reshape(-1)
