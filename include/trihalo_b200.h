@@ -28,6 +28,8 @@
  *                            reference, which is single-process).
  *   th_operator_source_box   the source cells an operator's kernels read for
  *                            one segment / half (the box a cross face ships).
+ *   th_pseudoinverse_rows    solve_pseudoinverse_rows (linalg.py:99-112), the
+ *                            builder's least-squares fit (build_derivative_fit).
  *
  * Conventions
  *   - Cell data are AoS: the u unknowns of a cell are contiguous (stride 1),
@@ -157,8 +159,11 @@ int32_t th_operator_export_rows(const th_operator* op, int32_t selector, int64_t
 
 /* Apply the operator to n_faces faces.  faces points to DEVICE memory
  * (n_faces th_face records).  `flag`, if not NULL, is a device int32 that is
- * OR-ed with 1 when any produced value is non-finite (the reference raises
- * ContractViolationError for non-finite sources, schemes.py:186). */
+ * OR-ed with 1 when a non-finite source value feeds the faces (the reference raises
+ * ContractViolationError for non-finite sources, schemes.py:186).  The interpolation kernels
+ * check each source slice through its first Gram moment (a plain sum), so finite inputs whose
+ * sum overflows (|v| ~ 1e307) are flagged too; the restriction kernels check every produced
+ * value.  th_check_finite checks values one by one. */
 int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, const th_face* faces,
                        int64_t n_faces, int32_t u, int32_t* flag, void* stream);
 
@@ -185,10 +190,20 @@ int32_t th_copy_box_layers(const double* src, double* dst, int64_t n_faces, int3
  * patches of the same level).  Face f copies the n_ext x t_ext x t_ext world box of
  * cells (n_ext along faces[f].normal) at src + faces[f].src[0] (world strides
  * faces[f].src_stride) to dst + faces[f].dst (strides faces[f].dst_stride), u unknowns
- * per cell, unknown stride 1.  Bit-exact copy; src and dst may be the same pool when
- * the boxes do not overlap.  All pointers device. */
+ * per cell, unknown stride 1.  Bit-exact copy.  src and dst may be the same pool when no
+ * face's target box overlaps ANY face's source box of the same launch (the kernel reads
+ * through the non-coherent path while other faces write): pool_same_level_faces with
+ * 1 <= k <= p satisfies it (halo layers are written, interior layers read).  All pointers
+ * device. */
 int32_t th_copy_faces(const double* src, double* dst, const th_face* faces, int64_t n_faces, int32_t n_ext,
                       int32_t t_ext, int32_t u, void* stream);
+
+/* Least-squares pseudo-inverse rows of a full-rank tall s x n matrix (host, row-major):
+ * w (n x s, row-major) = R^-1 Q^T from a Householder QR without pivoting, *cond = max|R_ii| /
+ * min|R_ii|; TH_ERR_SINGULAR (th_last_error_column() = column) when a pivot is below 1e-12 of
+ * the largest, TH_ERR_CONTRACT for s < n or non-finite entries.  The builder's own fit
+ * (linalg.py:40-112 solve_pseudoinverse_rows), exported for build_derivative_fit. */
+int32_t th_pseudoinverse_rows(const double* a, int32_t s, int32_t n, double* w, double* cond);
 
 /* Asynchronous byte copy on `stream`: kind 0 host->device, 1 device->host, 2 device->device
  * (host memory pinned or registered).  Moves patch pools and results between host buffers and

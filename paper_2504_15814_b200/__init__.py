@@ -46,6 +46,23 @@ from .schemes import (
     scheme_feasible,
 )
 from .faces import FaceBatch, copy_faces, pool_interp_faces, pool_restrict_faces, pool_same_level_faces, slab_faces
+from .construction import (
+    AxisOperator,
+    DerivativeFit,
+    StencilSpec,
+    TaylorBasis,
+    apply_tensor_interpolate,
+    apply_tensor_restrict,
+    build_axis_normal,
+    build_axis_tangential,
+    build_derivative_fit,
+    build_interpolation,
+    build_restriction,
+    collapse_to_matrix,
+    nearest_source_cell,
+    select_stencil,
+    taylor_basis,
+)
 from .csrio import dump_operator, dumps_operator, extract_half, extract_segment, from_triplets, load_operator
 from .harness import (
     BenchReport,

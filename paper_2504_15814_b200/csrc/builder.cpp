@@ -299,6 +299,10 @@ void choose_fast_path(HostOperator& op) {
 
 }  // namespace
 
+std::vector<double> fit_pseudo_inverse(const std::vector<double>& a, int s, int n, double& cond) {
+  return pseudo_inverse(a, s, n, cond);
+}
+
 void check_feasible(int role, int scheme, int p, int k) {
   if (scheme < 0 || scheme > 3)
     throw Error(Err::Config, "unknown scheme " + std::to_string(scheme) +

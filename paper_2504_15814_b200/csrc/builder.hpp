@@ -84,6 +84,10 @@ void check_feasible(int role, int scheme, int p, int k);
 
 HostOperator build_operator(int role, int scheme, int p, int k);
 
+// Householder QR least-squares pseudo-inverse of a full-rank tall s x n matrix (row-major),
+// rank test 1e-12 (linalg.py:40-112); returns n x s row-major, throws Error(Singular).
+std::vector<double> fit_pseudo_inverse(const std::vector<double>& a, int s, int n, double& cond);
+
 // CSR-style export of a row block (segment for interpolation: -1 = full
 // face; half for restriction), reference row order and column numbering.
 void export_rows(const HostOperator& op, int selector, std::vector<int64_t>& row_offsets,

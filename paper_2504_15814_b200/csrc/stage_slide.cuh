@@ -194,7 +194,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   extern __shared__ __align__(128) double sm[];
   double* const stages = sm;                                                      // [NST][stage_d]
   double* const wtab = sm + NST * stage_d;                  // ROLE 1: [class pair][z][y][a] folded weights
-  double* const rings = wtab + (ROLE == 1 ? op.st_ncls * op.st_ncls * 100 : 0);   // ROLE 0: [NCW][L][NT][32]
+  // ROLE 1: 20 zeros after the table, the weights of a t2 window a slice does not reach
+  double* const wzero = wtab + op.st_ncls * op.st_ncls * 100;
+  double* const rings = wtab + (ROLE == 1 ? op.st_ncls * op.st_ncls * 100 + 20 : 0);  // ROLE 0: [NCW][L][NT][32]
   double* const outbuf = rings + (ROLE == 0 ? NCW * L * NT * 32 : 0);             // ROLE 0: [out_d] output runs
   int* const hdr = reinterpret_cast<int*>(outbuf + (ROLE == 0 ? out_d : 0));      // [NST][4]
   unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);             // [NST][ny_max]
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   if constexpr (ROLE == 1) {
     // W_a(y, z) of every (t1, t2) synthesis-row class pair (host-built, trihalo.cu prepare_stage)
     for (int i = threadIdx.x; i < op.st_ncls * op.st_ncls * 100; i += blockDim.x) wtab[i] = __ldg(op.st_w + i);
+    for (int i = threadIdx.x; i < 20; i += blockDim.x) wzero[i] = 0.0;
   }
   __syncthreads();
 
@@ -446,8 +449,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
           const int XS = h[0], YS = h[1], BASE = h[2];
           const double* st = stages + size_t(s) * stage_d + BASE + cb + lane;
           const unsigned* el = eline + s * ny_max + ly;
-          const double* wa = wrow + cA * 100 + (inA ? zA : 0) * 20;
-          const double* wb = wrow + cB * 100 + (inB ? zB : 0) * 20;
+          // a window the slice does not reach reads the zero block; lanes past u read whatever
+          // follows their cell in the stage (finite or not: those results are never stored or
+          // checked, and the reads stay inside the shared allocation)
+          const double* wa = inA ? wrow + cA * 100 + zA * 20 : wzero;
+          const double* wb = inB ? wrow + cB * 100 + zB * 20 : wzero;
 #pragma unroll
           for (int y = 0; y < L; ++y) {
             const unsigned e = el[y];
@@ -455,14 +461,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
             double WA[D], WB[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-              WA[i] = inA ? wa[y * 4 + i] : 0.0;
-              WB[i] = inB ? wb[y * 4 + i] : 0.0;
+              WA[i] = wa[y * 4 + i];
+              WB[i] = wb[y * 4 + i];
             }
 #pragma unroll
             for (int q = 0; q < NU; ++q) {
               double v[L], m[D];
 #pragma unroll
-              for (int x = 0; x < L; ++x) v[x] = ok[q] ? ln[x * XS + int((e >> (6 * x)) & 63u) + 32 * q] : 0.0;
+              for (int x = 0; x < L; ++x) v[x] = ln[x * XS + int((e >> (6 * x)) & 63u) + 32 * q];
               gram_moments<L, D>(v, m);
 #pragma unroll
               for (int i = 0; i < D; ++i) {

@@ -44,8 +44,9 @@ struct Tile3Hdr {
   int g0, g1, n1, g2, n2;
   int y0, ny, z0, nz;  // the box along t1 / t2
   int cb, cn;          // the tile's unknowns [cb, cb + cn)
-  unsigned n1mag, cnmag;
+  unsigned n1mag, cnmag, nymag;
   int narrow;          // every target offset inside the face fits 32 bits
+  int4 G0;             // the normal group (window start, length, first target, children)
 };
 
 // 4 table doubles through two 16-byte shared-memory loads (p 16-byte aligned)
@@ -103,9 +104,11 @@ __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __r
     H.nz = __ldg(&op.grp1[H.g2 + H.n2 - 1]).x + 5 - H.z0;
   }
   const int4 G0 = __ldg(&op.grp0[fr.g0]);
+  H.G0 = G0;
   H.src_off = fr.src0 + int64_t(G0.x) * fr.sn + int64_t(H.y0) * fr.s1 + int64_t(H.z0) * fr.s2 + H.cb;
   H.n1mag = recip16(H.n1);
   H.cnmag = recip16(max(H.cn, 1));
+  H.nymag = recip16(max(H.ny, 1));
   const int64_t lim = int64_t(1) << 21;
   auto small = [lim](int64_t s) { return s > -lim && s < lim; };
   H.narrow = small(fr.dn) && small(fr.d1) && small(fr.d2) && op.p <= 64 && u <= (1 << 20);
@@ -119,7 +122,7 @@ __device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __r
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane >= H.cn) return;
   const int ny = H.ny, nl = H.ny * H.nz;
-  const unsigned nymag = recip16(max(ny, 1));
+  const unsigned nymag = H.nymag;
   const int64_t sn = H.sn, s1 = H.s1, s2 = H.s2;
   const double* const base = src + (H.src_off + lane);
   double* const bq = box + lane * T3BOX;
@@ -139,7 +142,7 @@ __device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const doubl
   const int n = H.ny * H.nz * 5;
   if (H.cn <= 0) return;
   const int last = H.cn * 8 - 1, ny = H.ny;
-  const unsigned nymag = recip16(max(ny, 1));
+  const unsigned nymag = H.nymag;
   const char* const base = reinterpret_cast<const char*>(src + H.src_off);
 #pragma unroll 1
   for (int c = threadIdx.x; c < n; c += NTH) {
@@ -266,7 +269,7 @@ template <int NTH, typename OFF>
 __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op, double* __restrict__ dst,
                                               const double* tr, const double* stab, const T3Syn0& s0,
                                               const int4* sgrp) {
-  const int4 G0 = __ldg(&op.grp0[H.g0]);
+  const int4 G0 = H.G0;
   bool ok0[3];
   OFF do0[3];
   bool all0 = true;
@@ -308,7 +311,7 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
 // dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (a [G0][12] slot, unused here: the
 // normal table is the kernel parameter syn0) | box[cmax][T3BOX] (+1 to an even count) | T[cmax][T3TP]
 template <int NTH, int MINB>
-__global__ void __launch_bounds__(NTH, MINB)
+__global__ void __launch_bounds__(NTH) __maxnreg__(65536 / (NTH * MINB) / 8 * 8)
     tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
                         const th_face* __restrict__ faces, int64_t n_tiles, int nt, int nch, int align, int cmax, int u,
                         int32_t* flag) {

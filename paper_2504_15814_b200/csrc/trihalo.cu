@@ -625,7 +625,7 @@ bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
     }
   g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
   const int NT = h.scheme == TH_SCHEME_TENSOR_LINEAR ? 9 : (L == 3 ? 6 : 10);
-  const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : op->st_w.size() * 8;
+  const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : op->st_w.size() * 8 + 20 * 8;
   // interpolation output staging (TMA bulk stores of contiguous target runs): one block row of
   // <= 3 normal x 3 tg t1 x 3 t2 children; TH_STAGE_OUT=0 disables (direct stores)
   static const int stage_out = [] { const char* e = std::getenv("TH_STAGE_OUT"); return e ? std::atoi(e) : 1; }();
@@ -1210,6 +1210,23 @@ int32_t th_memcpy_async(void* dst, const void* src, int64_t bytes, int32_t kind,
   if (!src || !dst) return fail(TH_ERR_CONTRACT, "NULL pointer");
   const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   TH_CUDA(cudaMemcpyAsync(dst, src, size_t(bytes), k, static_cast<cudaStream_t>(stream)));
+  return TH_OK;
+}
+
+int32_t th_pseudoinverse_rows(const double* a, int32_t s, int32_t n, double* w, double* cond) {
+  if (!a || !w || !cond) return fail(TH_ERR_CONFIG, "NULL argument");
+  if (n < 1 || s < n)
+    return fail(TH_ERR_CONTRACT, "system must have rows >= cols, got (" + std::to_string(s) + ", " + std::to_string(n) + ")");
+  for (int64_t i = 0; i < int64_t(s) * n; ++i)
+    if (!std::isfinite(a[i])) return fail(TH_ERR_CONTRACT, "matrix entries must be finite");
+  try {
+    double c = 0.0;
+    const std::vector<double> out = th::fit_pseudo_inverse(std::vector<double>(a, a + int64_t(s) * n), s, n, c);
+    std::copy(out.begin(), out.end(), w);
+    *cond = c;
+  } catch (const th::Error& e) {
+    return fail(map_error(e), e.what(), e.column);
+  }
   return TH_OK;
 }
 

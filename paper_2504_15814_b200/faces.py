@@ -181,10 +181,17 @@ def pool_same_level_faces(p: int, k: int, u: int, src_ids, dst_ids, normals, sid
     [p + k, p + 2k) <- neighbour interior [k, 2k).  Apply with ``copy_faces(pool, pool,
     rec, k, p, u)``; the boxes never overlap (halo vs interior cells).
     """
+    from .geometry import validate_pk
+
+    validate_pk(p, k)  # k <= p: the k interior source layers never reach the halo layers other faces write
     normals = np.asarray(normals, dtype=np.int64).ravel()
     sides = np.asarray(sides, dtype=np.int64).ravel()
     src_ids = np.asarray(src_ids, dtype=np.int64).ravel()
     dst_ids = np.asarray(dst_ids, dtype=np.int64).ravel()
+    if src_ids.size and (src_ids.min() < 0 or dst_ids.min() < 0):
+        raise ContractViolationError("patch ids must be >= 0")
+    if not (normals.size == sides.size == src_ids.size == dst_ids.size):
+        raise ContractViolationError("src_ids, dst_ids, normals and sides must have one entry per face")
     n = normals.size
     _, patch, strides = pool_geometry(p, k, u)
     rec = _records(n)
@@ -202,14 +209,22 @@ def copy_faces(src, dst, records, n_ext: int, t_ext: int, u: int, stream=None) -
     import torch
 
     lib = _native.load()
-    if isinstance(records, np.ndarray):
-        records = torch.from_numpy(records.view(np.uint8).ravel().copy()).to(src.device)
-    n = records.numel() // _native.FACE_DTYPE.itemsize
     for t in (src, dst):
         if not (t.is_cuda and t.dtype == torch.float64):
             raise ContractViolationError("copy_faces needs float64 CUDA tensors")
-    s = torch.cuda.current_stream(src.device).cuda_stream if stream is None else stream
-    _native.check(lib.th_copy_faces(src.data_ptr(), dst.data_ptr(), records.data_ptr(), n, n_ext, t_ext, u, s))
+    with torch.cuda.device(src.device):
+        if isinstance(records, np.ndarray):
+            records = torch.from_numpy(records.view(np.uint8).ravel().copy()).to(src.device)
+        n = records.numel() // _native.FACE_DTYPE.itemsize
+        if stream is None:
+            s = torch.cuda.current_stream(src.device).cuda_stream
+        else:  # the records (possibly a temporary) stay allocated until the copy on `stream` ran
+            s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+            if hasattr(stream, "cuda_stream"):
+                records.record_stream(stream)
+            else:
+                records.record_stream(torch.cuda.ExternalStream(s, device=src.device))
+        _native.check(lib.th_copy_faces(src.data_ptr(), dst.data_ptr(), records.data_ptr(), n, n_ext, t_ext, u, s))
 
 
 class FaceBatch:

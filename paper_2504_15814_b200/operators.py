@@ -183,14 +183,23 @@ class OperatorCache:
                 op = self._ops.setdefault(key, built)
         return op
 
+    def host_operator(self, role: str, scheme: str, p: int, k: int) -> HostOperator:
+        """Host-built operator (no device upload): CSR views work without a GPU."""
+        key = ("host", role, scheme, p, k)
+        op = self._ops.get(key)
+        if op is None:
+            built = HostOperator(role, scheme, p, k)
+            with self._lock:
+                op = self._ops.setdefault(key, built)
+        return op
+
     def get(self, key: OperatorKey) -> CsrOperator:
-        """Reference-compatible: the CSR rows of the keyed row block."""
+        """Reference-compatible: the CSR rows of the keyed row block (host; no GPU needed)."""
         if key.scheme == "tensor_linear":
             raise ConfigurationError("tensor_linear is applied per axis and has no matrix form")
         op = self._csr.get(key)
         if op is None:
-            dev = self.device_operator(key.role, key.scheme, key.p, key.k)
-            built = dev.csr(segment=key.segment, half=key.half)
+            built = self.host_operator(key.role, key.scheme, key.p, key.k).csr(segment=key.segment, half=key.half)
             with self._lock:
                 op = self._csr.setdefault(key, built)
         return op

@@ -96,17 +96,45 @@ class HaloExchange:
         dev = torch.device("cuda", self.op.device)
         self._src = torch.empty(max(self.n_src, 1), dtype=torch.float64, device=dev)
         self._out = torch.empty(max(self.n_out, 1), dtype=torch.float64, device=dev)
+        # page-locked staging for host callers: one H2D, two kernels, one D2H of the result and
+        # the non-finite flag, ONE synchronisation per run
+        self._h_src = torch.empty(max(self.n_src, 1), dtype=torch.float64, pin_memory=True)
+        self._h_out = torch.empty(max(self.n_out, 1), dtype=torch.float64, pin_memory=True)
+        self._h_flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._h_src_np, self._h_out_np = self._h_src.numpy(), self._h_out.numpy()
 
     def make_buffers(self, rng: np.random.Generator | None = None):
         src = rng.standard_normal(self.n_src) if rng is not None else np.zeros(self.n_src)
         return src, np.zeros(self.n_out)
 
-    def run(self, src_values, out_values) -> None:
-        """out_values[:] = operator(src_values); numpy arrays or CUDA tensors (world layout)."""
+    def _device_check(self, t, n: int, what: str) -> None:
         import torch
 
-        on_device = isinstance(src_values, torch.Tensor) and src_values.is_cuda
-        if on_device:
+        if t.dtype != torch.float64 or not t.is_contiguous() or t.device != self._src.device:
+            raise ContractViolationError(f"{what} must be a contiguous float64 tensor on {self._src.device}, got "
+                                         f"{t.dtype} on {t.device} (contiguous={t.is_contiguous()})")
+        if t.numel() != n:
+            raise ContractViolationError(f"{what} needs {n} values, got {t.numel()}")
+
+    def run(self, src_values, out_values) -> None:
+        """out_values[:] = operator(src_values); numpy arrays or CUDA tensors (world layout).
+
+        Like the reference (schemes.py:185-202) the source is checked for non-finite values
+        before anything is written: the result is computed into the exchange's own buffer and
+        copied into ``out_values`` only after the check passed."""
+        import torch
+
+        out_dev = isinstance(out_values, torch.Tensor) and out_values.is_cuda
+        src_dev = isinstance(src_values, torch.Tensor) and src_values.is_cuda
+        if out_dev:
+            self._device_check(out_values, self.n_out, "output")
+        elif np.asarray(out_values).size != self.n_out:
+            raise ContractViolationError(f"output needs {self.n_out} values, got {np.asarray(out_values).size}")
+        if src_dev:
+            self._device_check(src_values, self.n_src, "source")
+        if not src_dev and not out_dev:
+            return self._run_host(src_values, out_values)
+        if src_dev:
             src_t = src_values
         else:
             src_np = np.asarray(src_values, dtype=np.float64)
@@ -114,31 +142,69 @@ class HaloExchange:
                 raise ContractViolationError(f"source needs {self.n_src} values, got {src_np.size}")
             self._src.copy_(torch.from_numpy(np.ascontiguousarray(src_np).reshape(-1)))
             src_t = self._src
-        if src_t.numel() != self.n_src:
-            raise ContractViolationError(f"source needs {self.n_src} values, got {src_t.numel()}")
-        out_dev = isinstance(out_values, torch.Tensor) and out_values.is_cuda
-        out_t = out_values if out_dev else self._out
         if self.n_out == 0:
             return
         # whole-source finiteness, as the reference checks before applying (schemes.py:186)
         stream = torch.cuda.current_stream().cuda_stream
         _native.check(_native.load().th_check_finite(src_t.data_ptr(), self.n_src, self.batch.flag.data_ptr(), stream))
-        self.batch.launch(src_t, out_t, check_flag=False)
+        self.batch.launch(src_t, self._out, check_flag=False)
         if self.batch.nonfinite():
             raise ContractViolationError("source buffer contains non-finite values")
-        if not out_dev:
-            host = out_t[: self.n_out].cpu().numpy()
-            np.copyto(np.asarray(out_values).reshape(-1), host)
+        if out_dev:
+            out_values.copy_(self._out[: self.n_out])
+        else:
+            np.copyto(np.asarray(out_values).reshape(-1), self._out[: self.n_out].cpu().numpy())
+
+    def _run_host(self, src_values, out_values) -> None:
+        """Host arrays in and out: staged through page-locked buffers, one sync."""
+        import torch
+
+        src_np = np.asarray(src_values, dtype=np.float64).reshape(-1)
+        if src_np.size != self.n_src:
+            raise ContractViolationError(f"source needs {self.n_src} values, got {src_np.size}")
+        if self.n_out == 0:
+            return
+        lib = _native.load()
+        stream = torch.cuda.current_stream(self._src.device)
+        s = stream.cuda_stream
+        np.copyto(self._h_src_np[: self.n_src], src_np)
+        _native.check(lib.th_memcpy_async(self._src.data_ptr(), self._h_src.data_ptr(), self.n_src * 8, 0, s))
+        flag = self.batch.flag
+        _native.check(lib.th_check_finite(self._src.data_ptr(), self.n_src, flag.data_ptr(), s))
+        self.batch.launch(self._src, self._out, stream=s, check_flag=False)
+        _native.check(lib.th_memcpy_async(self._h_out.data_ptr(), self._out.data_ptr(), self.n_out * 8, 1, s))
+        _native.check(lib.th_memcpy_async(self._h_flag.data_ptr(), flag.data_ptr(), 4, 1, s))
+        stream.synchronize()
+        if int(self._h_flag_np()[0]):
+            flag.zero_()
+            raise ContractViolationError("source buffer contains non-finite values")
+        np.copyto(np.asarray(out_values).reshape(-1), self._h_out_np[: self.n_out])
+
+    def _h_flag_np(self):
+        return self._h_flag.numpy()
 
 
-_EXCHANGES: dict = {}
+_EXCHANGES: dict = {}          # exchanges built with the default cache
+_EXCHANGES_BY_CACHE = None     # weak: an OperatorCache's exchanges die with it
+_EXCHANGE_LIMIT = 4096         # per cache: (orientation x segment / half x scheme x role) fits easily
 
 
 def _exchange(cfg, scheme, role, half, cache) -> HaloExchange:
-    key = (cfg, scheme, role, half, id(cache) if cache is not None else None)
-    ex = _EXCHANGES.get(key)
+    global _EXCHANGES_BY_CACHE
+    import weakref
+
+    if cache is None:
+        table = _EXCHANGES
+    else:
+        if _EXCHANGES_BY_CACHE is None:
+            _EXCHANGES_BY_CACHE = weakref.WeakKeyDictionary()
+        table = _EXCHANGES_BY_CACHE.setdefault(cache, {})
+    key = (cfg, scheme, role, half)
+    ex = table.get(key)
     if ex is None:
-        ex = _EXCHANGES[key] = HaloExchange(cfg, scheme, role, half=half, cache=cache)
+        if len(table) >= _EXCHANGE_LIMIT:
+            table.clear()
+        ex = table[key] = HaloExchange(cfg, scheme, role, half=half, cache=cache)
     return ex
 
 

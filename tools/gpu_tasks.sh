@@ -18,6 +18,20 @@ for task in "$@"; do
     c[1-4])     n=${task#c}; timeout 900 python bench.py --config $n --steps 20 --warmup 5 --no-e2e > gpurun_out/bench_c$n.json 2> gpurun_out/bench_c$n.err; tail -3 gpurun_out/bench_c$n.err
                 python tools/bench_brief.py gpurun_out/bench_c$n.json ;;
     torchrun2)  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/torchrun1.json 2> gpurun_out/torchrun1.err; tail -c 400 gpurun_out/torchrun1.json ;;
+    ncu_c5)     # launch list of the default bench (config 5) + one full-set capture of both kernels (config 5 at 1/8 scale)
+                cmd="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu"
+                timeout 600 $cmd > gpurun_out/ncu_plain.json 2> gpurun_out/ncu_plain.err &&
+                timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches_c5.csv $cmd > gpurun_out/ncu_list.log 2>&1
+                cmd8="python bench.py --scale 0.125 --steps 1 --warmup 1 --no-e2e --no-cpu"
+                timeout 600 $cmd8 > gpurun_out/ncu_plain8.json 2>&1 &&
+                timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"tile3_interp|stage_slide" -s 2 -c 2 -o gpurun_out/prof_c5 -f $cmd8 > gpurun_out/ncu_full.log 2>&1
+                tail -2 gpurun_out/ncu_full.log ;;
+    reftests)   # the reference's own tests against the drop-in (needs baseline/_ref/tests_ref, git-ignored)
+                timeout 1200 python tools/run_reference_tests.py baseline/_ref/tests_ref test_schemes.py -q > gpurun_out/reftests_schemes.log 2>&1; tail -3 gpurun_out/reftests_schemes.log
+                timeout 1800 python tools/run_reference_tests.py baseline/_ref/tests_ref test_acceptance.py -q -k "criterion_1 or criterion_2 or criterion_3 or criterion_4" > gpurun_out/reftests_acceptance.log 2>&1; tail -3 gpurun_out/reftests_acceptance.log
+                timeout 1800 python tools/run_reference_tests.py baseline/_ref/tests_ref -q -rf --ignore=baseline/_ref/tests_ref/test_cli.py > gpurun_out/reftests_all.log 2>&1; grep -E "^FAILED|passed|failed" gpurun_out/reftests_all.log | tail -30 ;;
+    latency)    timeout 1200 python tools/per_face_latency.py > gpurun_out/per_face_latency.json 2> gpurun_out/per_face_latency.err; tail -12 gpurun_out/per_face_latency.err ;;
+    refcpu)     timeout 1200 python tools/reference_cpu.py 256 > gpurun_out/reference_cpu.json 2> gpurun_out/reference_cpu.err; cat gpurun_out/reference_cpu.json ;;
     *)          echo "unknown task $task" ;;
   esac
 done
