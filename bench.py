@@ -42,6 +42,9 @@ def parse():
                     help="config 5: fraction of faces with one fine patch drawn from the whole pool (A/B, tests)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink patch / face counts (tuning runs only)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--passes", default=None,
+                    help="configs 1-4: override the (role:scheme,...) passes, e.g. interpolate:matrix_linear,"
+                         "restrict:matrix_linear (extra measurements; the default is BASELINE's)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunks", type=int, default=16, help="pipeline chunks of the e2e leg")
     ap.add_argument("--cpu-sample", type=int, default=512, help="faces per pass in the CPU reference arm's sample")
@@ -172,6 +175,8 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     wl = W.build(args.config, rank=rank, scale=args.scale)
     s = wl.spec
+    if args.passes:
+        s.passes = [tuple(x.split(":")) for x in args.passes.split(",")]
     p, k, u = s.p, s.k, s.u
     passes = []
     cache = th.operators.DEFAULT_CACHE

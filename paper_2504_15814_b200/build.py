@@ -30,23 +30,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    out = out or OUT
+    if out == OUT and not force and not _stale():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *[os.path.join(CSRC, f) for f in SOURCES], "-o", OUT + ".tmp"]
+    extra = os.environ.get("TH_EXTRA_NVCC_FLAGS", "").split()  # A/B builds only (e.g. -DTH_AB_DMMA)
+    cmd = [nvcc, *NVCC_FLAGS, *extra, *[os.path.join(CSRC, f) for f in SOURCES], "-o", out + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed ({res.returncode})")
-    with open(os.path.join(os.path.dirname(OUT), "ptxas.log"), "w") as fh:
+    with open(os.path.join(os.path.dirname(out), "ptxas.log"), "w") as fh:
         fh.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_2504_15814_b200.build [--force] [--out PATH]   (TH_EXTRA_NVCC_FLAGS for A/B builds)
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose=True, out=o))

@@ -265,6 +265,103 @@ __device__ __forceinline__ void tile3_item(const double* tq, const T3Syn0& s0, c
   }
 }
 
+#ifdef TH_AB_DMMA
+// A/B variant (build with -DTH_AB_DMMA; profiles/r02_ab_dmma.txt): the synthesis of phase B on
+// the FP64 tensor cores.  Per block the children x moments matrix Syn[ch][mi] = S0[i][a] S1[j][b]
+// S2[l][c] (27 x 20, rows padded to 32) multiplies the moments of 8 unknowns at a time:
+// mma.sync.m8n8k4.f64 (one DMMA.8x8x4 per instruction on sm_100a), A = Syn tile (row = child),
+// B = moments (row = moment, column = unknown), 4 row tiles x 5 k-steps per group of 8 unknowns.
+// The z moments are computed as in tile3_item (lane = unknown) and reach the B fragments
+// through shuffles.
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename OFF>
+__device__ __forceinline__ void tile3_item_dmma(const double* tq, const T3Syn0& s0, const double* r1,
+                                                const double* r2, double* __restrict__ hdst, OFF qo0, OFF d1, OFF d2,
+                                                const OFF (&do0)[3], const bool (&ok0)[3], const bool (&ok1)[3],
+                                                const bool (&ok2)[3], int cn) {
+  constexpr int MO[10] = {0, 4, 7, 9, 10, 13, 15, 16, 18, 19};
+  constexpr int MN[10] = {4, 3, 2, 1, 3, 2, 1, 2, 1, 1};
+  const int lane = threadIdx.x & 31, n = lane >> 2, kq = lane & 3;
+  double M[20];
+#pragma unroll
+  for (int t = 0; t < 10; t += 2) {
+    double ca[5], cb[5];
+#pragma unroll
+    for (int z = 0; z < 5; ++z) {
+      const double2 v = *reinterpret_cast<const double2*>(tq + 10 * z + t);
+      ca[z] = v.x;
+      cb[z] = v.y;
+    }
+    gram_moments_n<5>(ca, M + MO[t], MN[t]);
+    gram_moments_n<5>(cb, M + MO[t + 1], MN[t + 1]);
+  }
+  // (a, b, c) of moment mi, 2 bits each, packed: mi -> bits [6 mi, 6 mi + 6)
+  constexpr unsigned long long PK_LO = [] {
+    unsigned long long v = 0;
+    int mi = 0;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; a + b < 4; ++b)
+        for (int c = 0; a + b + c < 4; ++c, ++mi)
+          if (mi < 10) v |= (unsigned long long)(a | (b << 2) | (c << 4)) << (6 * mi);
+    return v;
+  }();
+  constexpr unsigned long long PK_HI = [] {
+    unsigned long long v = 0;
+    int mi = 0;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; a + b < 4; ++b)
+        for (int c = 0; a + b + c < 4; ++c, ++mi)
+          if (mi >= 10) v |= (unsigned long long)(a | (b << 2) | (c << 4)) << (6 * (mi - 10));
+    return v;
+  }();
+  double A[4][5];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int ch = 8 * r + n;  // child (i, j, l), i fastest
+    const int l = ch / 9, j = (ch / 3) % 3, i = ch % 3;
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      const int mi = 4 * st + kq;
+      const unsigned e = unsigned((mi < 10 ? PK_LO >> (6 * mi) : PK_HI >> (6 * (mi - 10))) & 63u);
+      const int a = e & 3, b = (e >> 2) & 3, c = e >> 4;
+      A[r][st] = ch < 27 ? s0.v[i * 4 + a] * r1[j * 4 + b] * r2[l * 4 + c] : 0.0;
+    }
+  }
+#pragma unroll 1
+  for (int g = 0; g * 8 < cn; ++g) {
+    const int srcl = 8 * g + n;
+    double B[5];
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      const double v0 = __shfl_sync(0xffffffffu, M[4 * st + 0], srcl);
+      const double v1 = __shfl_sync(0xffffffffu, M[4 * st + 1], srcl);
+      const double v2 = __shfl_sync(0xffffffffu, M[4 * st + 2], srcl);
+      const double v3 = __shfl_sync(0xffffffffu, M[4 * st + 3], srcl);
+      B[st] = kq == 0 ? v0 : kq == 1 ? v1 : kq == 2 ? v2 : v3;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double C[2] = {0.0, 0.0};
+#pragma unroll
+      for (int st = 0; st < 5; ++st) dmma884(C, A[r][st], B[st]);
+      const int ch = 8 * r + n;
+      const int l = ch / 9, j = (ch / 3) % 3, i = ch % 3;
+      if (ch < 27 && ok0[i] && ok1[j] && ok2[l]) {
+        const int q = 8 * g + 2 * kq;
+        const OFF o = qo0 + OFF(q) + OFF(l) * d2 + OFF(j) * d1 + do0[i];
+        if (q < cn) *elem(hdst, o) = C[0];
+        if (q + 1 < cn) *elem(hdst, o + 1) = C[1];
+      }
+    }
+  }
+}
+#endif
+
 template <int NTH, typename OFF>
 __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op, double* __restrict__ dst,
                                               const double* tr, const double* stab, const T3Syn0& s0,
@@ -286,6 +383,25 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
   double* const hdst = dst + H.dst_off;
   // item (block, q) = (warp, lane): table reads are broadcasts, T reads conflict-free
   const int blk = threadIdx.x >> 5, q = threadIdx.x & 31;
+#ifdef TH_AB_DMMA
+  if (blk < n1 * H.n2) {  // whole warps: mma.sync
+    const int b2 = int((unsigned(blk) * H.n1mag) >> 16);
+    const int b1 = blk - b2 * n1;
+    const int g1 = g1b + b1, g2 = g2b + b2;
+    const int4 G1 = sgrp[g1], G2 = sgrp[g2];
+    bool ok1[3], ok2[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      ok1[j] = j < G1.w && unsigned(G1.z + j - lo1) < unsigned(p);
+      ok2[j] = j < G2.w && unsigned(G2.z + j - lo2) < unsigned(p);
+    }
+    const int qc = min(q, H.cn - 1);  // lanes past the chunk read a valid unknown's T
+    const double* tq = tr + (qc * T3TP + (G1.x - y0) * (10 * T3Y) + 10 * (G2.x - z0));
+    const OFF qo0 = OFF(G1.z - lo1) * d1 + OFF(G2.z - lo2) * d2 + OFF(cb);
+    tile3_item_dmma<OFF>(tq, s0, stab + g1 * 12, stab + g2 * 12, hdst, qo0, d1, d2, do0, ok0, ok1, ok2, H.cn);
+  }
+  return;
+#endif
   if (blk < n1 * H.n2 && q < H.cn) {
     const int b2 = int((unsigned(blk) * H.n1mag) >> 16);
     const int b1 = blk - b2 * n1;
@@ -310,8 +426,11 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
 
 // dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (a [G0][12] slot, unused here: the
 // normal table is the kernel parameter syn0) | box[cmax][T3BOX] (+1 to an even count) | T[cmax][T3TP]
+// 96 registers: 2 CTAs of 9 warps per SM need <= 5 warps per SM sub-partition (16 K registers
+// each), i.e. <= 3,276 registers per warp; at 104 / 112 registers only one CTA fits (measured:
+// fewer spills, slower)
 template <int NTH, int MINB>
-__global__ void __launch_bounds__(NTH) __maxnreg__(65536 / (NTH * MINB) / 8 * 8)
+__global__ void __launch_bounds__(NTH, MINB)
     tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
                         const th_face* __restrict__ faces, int64_t n_tiles, int nt, int nch, int align, int cmax, int u,
                         int32_t* flag) {

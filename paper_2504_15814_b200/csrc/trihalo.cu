@@ -515,7 +515,10 @@ void prepare_tile(th_operator* op) {
   op->ti_mode = 0;
   if (h.role != 0 || h.groups[0].size() != 1 || h.groups[1].empty()) return;
   int mode = 0;
-  if (h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) mode = 1;
+  // tensor_linear, and matrix_linear: its operator is the collapsed product of the same 1-D
+  // rows (linear.py:202-245), evaluated here in factored form (weights equal up to rounding)
+  const bool linear_rows = h.fast_mode == 2 || (h.fast_mode == 1 && h.scheme == TH_SCHEME_MATRIX_LINEAR);
+  if (linear_rows && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3) mode = 1;
   else if (h.gram_ok && h.fast_C0 == 3 && h.scheme == TH_SCHEME_ORDER2 && !h.synth[1].empty()) mode = 2;
   if (!mode) return;
   const th::Group& g0 = h.groups[0][0];
@@ -539,8 +542,7 @@ void prepare_tile(th_operator* op) {
   }
   // one tile per face only: at p = 17 (3 x 3 tiles of partial blocks) the per-warp slide is
   // faster (config 4 order2 interpolation 0.56 vs 0.43-0.49 of HBM, profiles/r01_ab_tile.txt)
-  static const bool multi = [] { const char* e = std::getenv("TH_TILE_MULTI"); return e && std::atoi(e); }();
-  if (nt > 1 && !multi) return;
+  if (nt > 1) return;
   op->ti_mode = mode;
   op->ti_nt = nt;
 }
@@ -585,63 +587,40 @@ struct StageGeom {
   size_t smem = 0;
 };
 constexpr int kRestrictNCW = 9, kRestrictNU = 2;  // restriction: one consumer warp per t1 group at u <= 64
-constexpr int kInterpNCW = 6;                      // interpolation: 3 t1 groups x 2 chunks of 32 at u <= 64
 
 bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   const th::HostOperator& h = op->host;
-  const bool interp = h.role == 0;
-  if (interp) {
-    if (h.groups[0].size() != 1 || h.fast_C0 != 3 || h.fast_CT != 3) return false;
-    const bool tensor = h.scheme == TH_SCHEME_TENSOR_LINEAR && h.fast_mode == 2 && h.fast_L0 == 3;
-    const bool gram = (h.scheme == TH_SCHEME_ORDER2 || h.scheme == TH_SCHEME_ORDER3) && h.gram_ok && h.fast_mode == 3;
-    if (!tensor && !gram) return false;
-  } else if (!op->st_ok) {
-    return false;
-  }
+  if (h.role != 1 || !op->st_ok) return false;
   const int L = h.fast_L0 > 0 ? h.fast_L0 : 5;
-  const int ncw = interp ? kInterpNCW : kRestrictNCW, nu = interp ? 1 : kRestrictNU;
+  const int ncw = kRestrictNCW, nu = kRestrictNU;
   const int nch = (u + 32 * nu - 1) / (32 * nu);
   if (nch > ncw) return false;
   const auto& g1 = h.groups[1];
-  // t1 group ranges a tile may come from: the three segment columns (interpolation) or the face
-  std::vector<std::pair<int, int>> ranges;
-  if (interp) {
-    for (int sgi = 0; sgi < 3; ++sgi)
-      if (h.seg_g[sgi][1] > h.seg_g[sgi][0]) ranges.push_back({h.seg_g[sgi][0], h.seg_g[sgi][1]});
-  } else {
-    ranges.push_back({0, (int)g1.size()});
-  }
-  int max_n = 0;
-  for (auto& r : ranges) max_n = std::max(max_n, r.second - r.first);
+  const int max_n = (int)g1.size();
   if (max_n == 0) return false;
   const int tiles = (max_n + ncw / nch - 1) / (ncw / nch);
   g.tg = (max_n + tiles - 1) / tiles;
   g.tiles_per_face = tiles;
   g.ny_max = 0;
-  for (auto& r : ranges)
-    for (int ga = r.first; ga < r.second; ga += g.tg) {
-      const int gb = std::min(r.second, ga + g.tg);
-      g.ny_max = std::max(g.ny_max, g1[gb - 1].win0 + L - g1[ga].win0);
-    }
+  for (int ga = 0; ga < max_n; ga += g.tg) {
+    const int gb = std::min(max_n, ga + g.tg);
+    g.ny_max = std::max(g.ny_max, g1[gb - 1].win0 + L - g1[ga].win0);
+  }
+  // stage rows hold runs of u-double cells widened to 16-byte boundaries; lanes past u read up to
+  // 63 - u doubles beyond a cell (never stored), covered by the regions that follow the stages
   g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
-  const int NT = h.scheme == TH_SCHEME_TENSOR_LINEAR ? 9 : (L == 3 ? 6 : 10);
-  const size_t extra = interp ? size_t(ncw) * L * NT * 32 * 8 : op->st_w.size() * 8 + 20 * 8;
-  // interpolation output staging (TMA bulk stores of contiguous target runs): one block row of
-  // <= 3 normal x 3 tg t1 x 3 t2 children; TH_STAGE_OUT=0 disables (direct stores)
-  static const int stage_out = [] { const char* e = std::getenv("TH_STAGE_OUT"); return e ? std::atoi(e) : 1; }();
-  const int out_want = interp && stage_out ? ((3 * 3 * g.tg * 3 * (u + 3) + 1) & ~1) : 0;
+  const size_t extra = op->st_w.size() * 8 + 20 * 8;
   const size_t budget = size_t(227 * 1024) / size_t(minb) - 1024;
-  for (int out_d : {out_want, 0})
-    for (int nst = 3; nst >= 2; --nst) {
-      const size_t smem = size_t(nst) * g.stage_d * 8 + extra + size_t(out_d) * 8 + size_t(nst) * 16 +
-                          size_t(nst) * g.ny_max * 4 + size_t(L) * g.ny_max + 64;
-      if (smem <= budget) {
-        g.nst = nst;
-        g.smem = smem;
-        g.out_d = out_d;
-        return true;
-      }
+  for (int nst = 3; nst >= 2; --nst) {
+    const size_t smem = size_t(nst) * g.stage_d * 8 + extra + size_t(nst) * 16 + size_t(nst) * g.ny_max * 4 +
+                        size_t(L) * g.ny_max + 64 * 8;
+    if (smem <= budget) {
+      g.nst = nst;
+      g.smem = smem;
+      g.out_d = 0;
+      return true;
     }
+  }
   return false;
 }
 
@@ -903,24 +882,24 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     kfn<<<sblocks, (NCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,      \
                                                  sg.ny_max, sg.tg, sg.tiles_per_face, sg.out_d);              \
   } while (0)
-  // Kernel choice: the measured defaults (profiles/r01_ab_*.txt); register budgets are the
-  // largest occupancies at which the hot kernels do not spill.  Environment switches, read
-  // once per process, exist for A/B runs and are exercised by the GPU tests:
+  // Kernel choice: the measured defaults (profiles/r01_ab_*.txt, r02_*); register budgets are the
+  // largest occupancies at which the hot kernels do not spill.  Environment switches, read once
+  // per process, select the fallbacks for A/B runs and are exercised by the GPU tests:
   //   TH_GRAM bits (default 15)  1: Gram slide for order2 / order3 interpolation
   //                              2: Gram slide for order3 restriction (fallback of bit 4)
   //                              4: slice-staged order3 restriction (stage_slide.cuh)
   //                              8: tensor_linear interpolation through the slice ring
-  //   TH_STAGE_INTERP=1          slice-staged interpolation (off: no faster than the slide,
-  //                              interpolation is bound by its per-warp latency and its 472-byte
-  //                              cell stores, profiles/r01_ab_stage.txt, r01_probe_store.txt)
-  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 15; }();
-  static const int stage_interp = [] { const char* e = std::getenv("TH_STAGE_INTERP"); return e ? std::atoi(e) : 0; }();
-  const bool gram = h.gram_ok && h.fast_C0 == 3;
-  const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
   //   TH_TILE=0                  per-warp slide (gram_slide.cuh) instead of the tile-parallel
   //                              interpolation kernel (tile_interp.cuh)
+  //   TH_TILE3=0                 order3 interpolation through the per-warp slide instead of the
+  //                              staged two-phase tiles (tile_interp3.cuh)
+  // (Round 1's TH_STAGE_INTERP, TH_TILE_CFG, TH_TILE_MULTI and TH_TILE3=2 variants lost their
+  // A/Bs and were removed.)
+  static const int use_gram = [] { const char* e = std::getenv("TH_GRAM"); return e ? std::atoi(e) : 15; }();
+  const bool gram = h.gram_ok && h.fast_C0 == 3;
+  const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
   static const int use_tile = [] { const char* e = std::getenv("TH_TILE"); return e ? std::atoi(e) : 1; }();
-  if (use_tile && interp && op->ti_mode && !stage_interp) {
+  if (use_tile && interp && op->ti_mode) {
     const int nt = op->ti_nt;
     const int pitch = TBOX | 1;
     const int TW = op->ti_mode == 1 ? 9 : 12;
@@ -938,27 +917,15 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));          \
     kfn<<<tblocks, NTH, smem, s>>>(op->dev, src, dst, faces, tiles, nt, pitch, u, umag, flag);              \
   } while (0)
-      // TH_TILE_CFG (A/B): 0 = 192 threads x 2 CTAs/SM (default), 1 = 192 x 3, 2 = 256 x 2
-      static const int tcfg = [] { const char* e = std::getenv("TH_TILE_CFG"); return e ? std::atoi(e) : 0; }();
-      if (op->ti_mode == 1) {
-        if (tcfg == 1) TH_TILEK(true, 192, 3);
-        else if (tcfg == 2) TH_TILEK(true, 256, 2);
-        else TH_TILEK(true, 192, 2);
-      } else {
-        if (tcfg == 1) TH_TILEK(false, 192, 3);
-        else if (tcfg == 2) TH_TILEK(false, 256, 2);
-        else TH_TILEK(false, 192, 2);
-      }
+      if (op->ti_mode == 1) TH_TILEK(true, 192, 2);
+      else TH_TILEK(false, 192, 2);
 #undef TH_TILEK
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
   }
-  //   TH_TILE3=0                 order3 interpolation through the per-warp slide instead of the
-  //                              staged two-phase tiles (tile_interp3.cuh)
   static const int use_tile3 = [] { const char* e = std::getenv("TH_TILE3"); return e ? std::atoi(e) : 1; }();
-  //   TH_TILE3=2                 also when a face splits into several spatial tiles (p = 17)
-  if (use_tile3 && interp && op->t3_ok && !stage_interp && (op->t3_nt == 1 || use_tile3 == 2)) {
+  if (use_tile3 && interp && op->t3_ok && op->t3_nt == 1) {
     // tiles = (face, chunk of <= T3CMAX unknowns); chunk boundaries on 4-unknown (32-byte)
     // sector edges when every chunk still fits
     const int nch = (u + T3CMAX - 1) / T3CMAX;
@@ -988,11 +955,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     }
   }
   StageGeom sg;
-  if (stage_interp && interp && stage_geometry(op, u, h.scheme == TH_SCHEME_ORDER3 ? 1 : 2, sg)) {
-    if (h.scheme == TH_SCHEME_ORDER3) TH_SLIDE(0, 3, false, kInterpNCW, 1, 1);
-    else if (h.scheme == TH_SCHEME_TENSOR_LINEAR) TH_SLIDE(0, 2, true, kInterpNCW, 1, 2);
-    else TH_SLIDE(0, 2, false, kInterpNCW, 1, 2);
-  } else if ((use_gram & 8) && interp && tensor_fast) {
+  if ((use_gram & 8) && interp && tensor_fast) {
     // tensor_linear interpolation through the slice ring (gram_slide.cuh, TENSOR = true)
     auto kfn = gram_slide_kernel<2, 0, 4, true>;
     const size_t smem = size_t(4) * 3 * 9 * 32 * 8;
@@ -1011,11 +974,13 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   else if (op->r_mode == 2 && op->r_L == 3) TH_RREG(2, 3, 1, 2, 4, 8);
   else if (op->r_mode == 1 && op->r_L == 5) TH_RREG(1, 5, 9, 2, 4, 8);
 #undef TH_RREG
-  else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0, 3);
-  else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0, 3);
-  else if (h.fast_mode == 2 && h.fast_L0 == 3 && interp) TH_WIN(2, 3, 3, 0, 1, 0, 3);
-  else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 2, 0, 3);
-  else if (h.fast_mode == 1 && h.fast_L0 == 3 && interp) TH_WIN(1, 3, 3, 0, 2, 0, 2);
+  // (occupancies: the largest at which each instantiation does not spill, ptxas.log)
+  else if (h.fast_mode == 3 && h.fast_L0 == 3 && interp) TH_WIN(3, 3, 3, 2, 1, 0, 2);
+  else if (h.fast_mode == 3 && h.fast_L0 == 5 && interp) TH_WIN(3, 5, 3, 3, 1, 0, 2);
+  else if ((h.fast_mode == 2 || (h.fast_mode == 1 && h.scheme == TH_SCHEME_MATRIX_LINEAR)) && h.fast_L0 == 3 &&
+           interp)
+    TH_WIN(2, 3, 3, 0, 1, 0, 2);  // d-linear rows (tensor_linear; matrix_linear in factored form)
+  else if (h.fast_mode == 2 && h.fast_L0 == 3 && !interp) TH_WIN(2, 3, 1, 0, 2, 0, 2);
   else if (h.fast_mode == 1 && h.fast_L0 == 3 && !interp && op->smem_ok) TH_WIN(1, 3, 1, 0, 2, op->smem_bytes, 2);
   else if (h.fast_mode == 1 && h.fast_L0 == 5 && !interp && op->smem_ok) TH_WIN(1, 5, 1, 0, 2, op->smem_bytes, 2);
   else done = false;

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(128, MINB) window_kernel(DevOp op, const doubl
         for (int c = 0; c < NM; ++c)
 #pragma unroll
           for (int q = 0; q < NU; ++q) acc[c][q] = 0.0;
-#pragma unroll(LT == 3 ? LT : 1)
+#pragma unroll((LT == 3 && MODE == 3) ? LT : 1)  // MODE 1 / 2: acc[CH] and a slice stay in registers
         for (int z = 0; z < LT; ++z) {
           double v[LT][L0][NU];
 #pragma unroll

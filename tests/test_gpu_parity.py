@@ -354,17 +354,14 @@ def test_pool_transposed_layout(th, scheme, p):
         assert np.array_equal(outs[0], outs[1]), (role, scheme, np.abs(outs[0] - outs[1]).max())
 
 
-@pytest.mark.parametrize("env", ({"TH_STAGE_INTERP": "1"}, {"TH_GRAM": "3"}, {"TH_TILE": "0"},
-                                 {"TH_TILE_MULTI": "1"}, {"TH_TILE_CFG": "2"},
-                                 {"TH_TILE3": "0"}, {"TH_TILE3": "2"}))
+@pytest.mark.parametrize("env", ({"TH_GRAM": "3"}, {"TH_TILE": "0"}, {"TH_TILE3": "0"},
+                                 {"TH_TILE": "0", "TH_GRAM": "0"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
-    parity tests in a child process with the alternative paths (slice-staged
-    interpolation; the per-warp order3 restriction slide; the per-warp interpolation
-    slide instead of the staged tile kernel; staged tiles also at p = 17, where a face
-    splits into 3 x 3 tiles of partial blocks; another tile CTA shape; the per-warp slide
-    for order3 interpolation instead of the two-phase order3 tiles; the two-phase tiles also
-    at p = 17, 3 x 3 spatial tiles per face)."""
+    parity tests in a child process with the alternative paths (the per-warp order3
+    restriction slide; the per-warp interpolation slide instead of the staged tile kernel;
+    the per-warp slide for order3 interpolation instead of the two-phase order3 tiles; the
+    fixed-window kernels with neither tiles nor Gram slides)."""
     import os
     import subprocess
     import sys
