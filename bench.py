@@ -42,6 +42,8 @@ def parse():
                     help="config 5: fraction of faces with one fine patch drawn from the whole pool (A/B, tests)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink patch / face counts (tuning runs only)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--graph", action="store_true",
+                    help="configs 1-4: capture the timed steps in one CUDA graph (launch-bound small batches)")
     ap.add_argument("--passes", default=None,
                     help="configs 1-4: override the (role:scheme,...) passes, e.g. interpolate:matrix_linear,"
                          "restrict:matrix_linear (extra measurements; the default is BASELINE's)")
@@ -232,16 +234,34 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    graph = None
+    if args.graph:  # the K timed steps as one CUDA graph: no host launch gaps between passes
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for kk in range(args.steps):
+                step()
+        torch.cuda.synchronize()
+        graph.replay()  # warm replay
+        torch.cuda.synchronize()
     sampler.mark()
     t0.record(stream)
-    for kk in range(args.steps):
-        step(ev_all[kk])
+    if graph is not None:
+        graph.replay()
+    else:
+        for kk in range(args.steps):
+            step(ev_all[kk])
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     clocks = sampler.stop()
     total_ms = t0.elapsed_time(t1)
+    if graph is not None:  # per-pass events from ungraphed steps (the graph has no event nodes)
+        for kk in range(args.steps):
+            step(ev_all[kk])
+        torch.cuda.synchronize()
     if side is not None:  # no per-pass events in the overlapped step: one serial step per pass row
         ev_all = ev_all[:1]
         step(None)

@@ -426,9 +426,10 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
 
 // dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (a [G0][12] slot, unused here: the
 // normal table is the kernel parameter syn0) | box[cmax][T3BOX] (+1 to an even count) | T[cmax][T3TP]
-// 96 registers: 2 CTAs of 9 warps per SM need <= 5 warps per SM sub-partition (16 K registers
-// each), i.e. <= 3,276 registers per warp; at 104 / 112 registers only one CTA fits (measured:
-// fewer spills, slower)
+// One CTA per SM (MINB = 1): no spills (126 registers).  Two CTAs per SM need <= 96 registers
+// (<= 5 warps per 16 K-register SM sub-partition) and spill ~200 bytes; on config 5 at full size
+// (196,608 faces over a 52 GB pool) one CTA per SM is 1.30x faster (11.1 vs 14.4 ms, same box,
+// same call; at 24,576 faces two CTAs are 3% faster): profiles/r02_ab_tile3_regs.txt.
 template <int NTH, int MINB>
 __global__ void __launch_bounds__(NTH, MINB)
     tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,

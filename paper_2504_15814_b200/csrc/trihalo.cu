@@ -943,7 +943,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int nt = op->t3_nt;
     const int64_t tiles = n_faces * int64_t(nt * nt * nch);
     if (smem <= 227 * 1024) {
-      auto kfn = tile3_interp_kernel<288, 2>;
+      auto kfn = tile3_interp_kernel<288, 1>;
       int per_sm = 0;
       TH_CUDA(resident_ctas(reinterpret_cast<const void*>(kfn), 288, smem, &per_sm));
       const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));

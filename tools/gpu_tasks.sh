@@ -32,6 +32,8 @@ for task in "$@"; do
                 timeout 1800 python tools/run_reference_tests.py baseline/_ref/tests_ref -q -rf --ignore=baseline/_ref/tests_ref/test_cli.py > gpurun_out/reftests_all.log 2>&1; grep -E "^FAILED|passed|failed" gpurun_out/reftests_all.log | tail -30 ;;
     latency)    timeout 1200 python tools/per_face_latency.py > gpurun_out/per_face_latency.json 2> gpurun_out/per_face_latency.err; tail -12 gpurun_out/per_face_latency.err ;;
     refcpu)     timeout 1200 python tools/reference_cpu.py 256 > gpurun_out/reference_cpu.json 2> gpurun_out/reference_cpu.err; cat gpurun_out/reference_cpu.json ;;
+    matrix)     timeout 900 python bench.py --config 2 --passes interpolate:matrix_linear,restrict:matrix_linear,interpolate:tensor_linear,restrict:tensor_linear --steps 20 --warmup 5 --no-e2e > gpurun_out/bench_matrix.json 2> gpurun_out/bench_matrix.err; tail -3 gpurun_out/bench_matrix.err
+                python tools/bench_brief.py gpurun_out/bench_matrix.json ;;
     *)          echo "unknown task $task" ;;
   esac
 done
