@@ -117,9 +117,11 @@ __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __r
 // cp.async copies of the tile's box into box[q][x + 5 (y + T3Y z)]: warps over the box's source
 // lines (y, z) (all 9 warps, so the copies are issued quickly), lanes over the chunk's unknowns
 template <int NTH>
-__device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __restrict__ src, double* box) {
+__device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __restrict__ src, double* box,
+                                            int warp = -1) {
   constexpr int NW = NTH / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp < 0) warp = threadIdx.x >> 5;
   if (lane >= H.cn) return;
   const int ny = H.ny, nl = H.ny * H.nz;
   const unsigned nymag = H.nymag;
@@ -138,14 +140,15 @@ __device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __r
 
 // L2 prefetch of a tile's box: one source cell per thread, the <= 3 128-byte lines of its chunk
 template <int NTH>
-__device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const double* __restrict__ src) {
+__device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const double* __restrict__ src, int tid = -1) {
   const int n = H.ny * H.nz * 5;
   if (H.cn <= 0) return;
+  if (tid < 0) tid = threadIdx.x;
   const int last = H.cn * 8 - 1, ny = H.ny;
   const unsigned nymag = H.nymag;
   const char* const base = reinterpret_cast<const char*>(src + H.src_off);
 #pragma unroll 1
-  for (int c = threadIdx.x; c < n; c += NTH) {
+  for (int c = tid; c < n; c += NTH) {
     const int r = int((unsigned(c) * 13108u) >> 16);  // c / 5 (exact for c < 16384)
     const int x = c - 5 * r;
     const int z = int((unsigned(r) * nymag) >> 16), y = r - z * ny;
@@ -158,9 +161,10 @@ __device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const doubl
 
 // phase A: item (z, q) -> T[q][s][z][t] for every window start s of the box (NY = box
 // extent along t1, compile-time so the line moments stay in registers)
-template <int NTH, int NY>
-__device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double* box, double* tr, double& chk) {
-  const int z = threadIdx.x >> 5, q = threadIdx.x & 31;
+template <int NY>
+__device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double* box, double* tr, double& chk,
+                                                 int z) {
+  const int q = threadIdx.x & 31;
   {
     const double* bz = box + q * T3BOX + 5 * T3Y * z;
     double mm[NY][4];
@@ -194,10 +198,24 @@ __device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double
 template <int NTH>
 __device__ __forceinline__ void tile3_phase_a(const Tile3Hdr& H, const double* box, double* tr, double& chk) {
   // item (z, q) = (warp, lane): conflict-free box / T accesses (odd pitches)
-  if ((threadIdx.x >> 5) >= H.nz || (threadIdx.x & 31) >= H.cn) return;
-  if (H.ny == 5) tile3_phase_a_ny<NTH, 5>(H, box, tr, chk);
-  else if (H.ny == 6) tile3_phase_a_ny<NTH, 6>(H, box, tr, chk);
-  else if (H.ny == 7) tile3_phase_a_ny<NTH, 7>(H, box, tr, chk);
+  const int z = threadIdx.x >> 5;
+  if (z >= H.nz || (threadIdx.x & 31) >= H.cn) return;
+  if (H.ny == 5) tile3_phase_a_ny<5>(H, box, tr, chk, z);
+  else if (H.ny == 6) tile3_phase_a_ny<6>(H, box, tr, chk, z);
+  else if (H.ny == 7) tile3_phase_a_ny<7>(H, box, tr, chk, z);
+}
+
+// phase A by a group of NW warps (warp w of the group takes slices z = w, w + NW, ...)
+template <int NW>
+__device__ __forceinline__ void tile3_phase_a_group(const Tile3Hdr& H, const double* box, double* tr, double& chk,
+                                                    int w) {
+  if ((threadIdx.x & 31) >= H.cn) return;
+#pragma unroll 1
+  for (int z = w; z < H.nz; z += NW) {
+    if (H.ny == 5) tile3_phase_a_ny<5>(H, box, tr, chk, z);
+    else if (H.ny == 6) tile3_phase_a_ny<6>(H, box, tr, chk, z);
+    else if (H.ny == 7) tile3_phase_a_ny<7>(H, box, tr, chk, z);
+  }
 }
 
 // phase B: item (block, q): z moments from T, synthesis at the children, stores
@@ -365,7 +383,7 @@ __device__ __forceinline__ void tile3_item_dmma(const double* tq, const T3Syn0& 
 template <int NTH, typename OFF>
 __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op, double* __restrict__ dst,
                                               const double* tr, const double* stab, const T3Syn0& s0,
-                                              const int4* sgrp) {
+                                              const int4* sgrp, int blk = -1) {
   const int4 G0 = H.G0;
   bool ok0[3];
   OFF do0[3];
@@ -382,7 +400,8 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
   const int cb = H.cb;
   double* const hdst = dst + H.dst_off;
   // item (block, q) = (warp, lane): table reads are broadcasts, T reads conflict-free
-  const int blk = threadIdx.x >> 5, q = threadIdx.x & 31;
+  if (blk < 0) blk = threadIdx.x >> 5;
+  const int q = threadIdx.x & 31;
 #ifdef TH_AB_DMMA
   if (blk < n1 * H.n2) {  // whole warps: mma.sync
     const int b2 = int((unsigned(blk) * H.n1mag) >> 16);
@@ -473,4 +492,99 @@ __global__ void __launch_bounds__(NTH, MINB)
   }
   cp_async_wait_all();
   raise_flag(flag, !isfinite(chk));
+}
+
+
+// ---------------------------------------------------------------------------
+// Warp-specialised variant: phase A and phase B of consecutive tiles run at the same time.
+//
+// The two-phase kernel above idles warps at every tile: phase A keeps <= 7 of 9 warps busy
+// and both phases end in a CTA barrier (ncu: barrier the top stall, 2.1 cycles per issue).
+// Here a CTA is NA3 "A" warps + 9 "B" warps.  A warps fetch (cp.async) and project tile i
+// into T[i % 2] while B warps synthesise tile i - 1 from T[(i - 1) % 2]; boxes and T are
+// double-buffered, and the hand-off uses named barriers (bar.arrive by the producer side,
+// bar.sync by the consumer side):
+//   A_BAR (id 1, A warps)       box i landed for every A thread / box i no longer read
+//   T_FULL[b] (ids 2, 3, all)   T[b] written (A arrive, B sync)
+//   T_EMPTY[b] (ids 4, 5, all)  T[b] consumed (B arrive, A sync before rewriting it)
+// A warps also decode the tile headers (ring of 8) and L2-prefetch the tile after next.
+// Same arithmetic as tile3_interp_kernel (results bitwise equal).
+// ---------------------------------------------------------------------------
+constexpr int NA3 = 4;                 // A warps
+constexpr int T3P_NTH = (NA3 + 9) * 32;
+constexpr int T3PCMAX = 30;            // unknowns per tile: 2 x (box + T) within 227 KB
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (unused [G0][12] slot) | box[2][cmax][T3BOX]
+// (each rounded to an even count) | T[2][cmax][T3TP]
+__global__ void __launch_bounds__(T3P_NTH, 1)
+    tile3p_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
+                         const th_face* __restrict__ faces, int64_t n_tiles, int nt, int nch, int align, int cmax,
+                         int u, int32_t* flag) {
+  extern __shared__ __align__(16) double smem_t3p[];
+  __shared__ Tile3Hdr Hs[8];
+  const int G1n = op.G1;
+  int4* const sgrp = reinterpret_cast<int4*>(smem_t3p);
+  double* const stab = smem_t3p + 2 * G1n;
+  const int boxd = (cmax * T3BOX + 1) & ~1, trd = cmax * T3TP;
+  double* const box0 = smem_t3p + tile_box_offset(12, op.G0, G1n);
+  double* const tr0 = box0 + 2 * boxd;
+  for (int i = threadIdx.x; i < G1n; i += T3P_NTH) sgrp[i] = __ldg(&op.grp1[i]);
+  for (int i = threadIdx.x; i < G1n * 12; i += T3P_NTH) stab[i] = __ldg(op.synth1 + i);
+  const int warp = threadIdx.x >> 5;
+  const int64_t t0 = blockIdx.x, step = gridDim.x;
+  constexpr int ALL = T3P_NTH, ANTH = NA3 * 32;
+  if (warp < NA3) {
+    // ============ A warps: fetch, phase A ============
+    const int atid = threadIdx.x;
+    if (atid == 0)
+      for (int i = 0; i < 4; ++i)
+        if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nt, nch, align, u, Hs[i]);
+    __syncthreads();  // (with the B warps: tables and headers 0..3 visible to everyone)
+    if (t0 < n_tiles) tile3_fetch<ANTH>(Hs[0], src, box0, warp);
+    cp_async_commit();
+    if (t0 + step < n_tiles) tile3_fetch<ANTH>(Hs[1], src, box0 + boxd, warp);
+    cp_async_commit();
+    if (t0 + 2 * step < n_tiles) tile3_prefetch_l2<ANTH>(Hs[2], src, atid);
+    double chk = 0.0;
+    int it = 0;
+    for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
+      const int b = it & 1;
+      cp_async_wait_one();
+      bar_sync_n(1, ANTH);                       // box b holds tile `it` for every A thread
+      if (it >= 2) bar_sync_n(4 + b, ALL);       // B is done with T[b] (tile it - 2)
+      if (atid == 0 && tile + 4 * step < n_tiles)  // Hs[(it + 4) & 7]: B is at tile >= it - 1
+        tile3_decode(op, faces, tile + 4 * step, nt, nch, align, u, Hs[(it + 4) & 7]);
+      const Tile3Hdr& H = Hs[it & 7];
+      tile3_phase_a_group<NA3>(H, box0 + b * boxd, tr0 + b * trd, chk, warp);
+      bar_arrive_n(2 + b, ALL);                  // T[b] ready
+      bar_sync_n(1, ANTH);                       // every A thread is done reading box b
+      if (tile + 2 * step < n_tiles) tile3_fetch<ANTH>(Hs[(it + 2) & 7], src, box0 + b * boxd, warp);
+      cp_async_commit();
+      if (tile + 3 * step < n_tiles) tile3_prefetch_l2<ANTH>(Hs[(it + 3) & 7], src, atid);
+    }
+    // drain: the B warps' T_EMPTY arrivals of the last two tiles have no matching sync yet
+    for (int k = it - 2; k < it; ++k)
+      if (k >= 0) bar_sync_n(4 + (k & 1), ALL);
+    cp_async_wait_all();
+    raise_flag(flag, !isfinite(chk));
+  } else {
+    // ============ B warps: phase B (warp = block of the 3 x 3 tile) ============
+    __syncthreads();
+    int it = 0;
+    for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
+      const int b = it & 1;
+      bar_sync_n(2 + b, ALL);                    // T[b] holds tile `it`
+      const Tile3Hdr& H = Hs[it & 7];
+      // phase B with the B warps renumbered 0..8 (tile3_phase_b maps warp -> block)
+      if (H.narrow) tile3_phase_b<T3P_NTH, int>(H, op, dst, tr0 + b * trd, stab, syn0, sgrp, warp - NA3);
+      else tile3_phase_b<T3P_NTH, int64_t>(H, op, dst, tr0 + b * trd, stab, syn0, sgrp, warp - NA3);
+      bar_arrive_n(4 + b, ALL);                  // T[b] consumed
+    }
+  }
 }
