@@ -6,20 +6,17 @@
 // discrete Gram polynomials), organised so that no source load sits on a thread's
 // critical path and the normal / t1 passes are shared by every block that needs them:
 //
-//  * a CTA owns a tile = (face, spatial tile of <= 3 x 3 blocks, chunk of <= 31 unknowns);
-//    the tile's source support (5 normal x <= 7 x <= 7 coarse cells: the whole segment at
-//    p <= 9; with TH_TILE3=2 a third of it per axis at p = 17) is copied into a
-//    shared-memory box with 8-byte cp.async, and the tile after next is L2-prefetched;
-//  * phase A, warp = t2 slice z, lane = unknown: the x (normal) Gram moments of the
-//    slice's <= 7 lines, then the y moments of each distinct t1 window start s (<= 3),
-//    written as T[s][z][pair] to a second shared region.  The box is then free: the NEXT
-//    tile's copy is issued before phase B, so it lands while phase B computes;
-//  * phase B, warp = block, lane = unknown: the block's z moments from its 5 T slices,
-//    the synthesis at its <= 27 children, direct stores (a warp writes contiguous runs of
-//    unknowns).
-// Two CTAs per SM (2 x 114 KB of shared memory) alternate between the phases; that
-// interleaving is what hides the barriers (one 18-warp CTA per SM measured 0.43 of HBM
-// against 0.58, profiles/r01_ab_tile3.txt).
+//  * a tile = (face, chunk of <= 30 unknowns); its source support (5 normal x <= 7 x <= 7
+//    coarse cells: the whole segment at p <= 9) is copied into a shared-memory box with
+//    8-byte cp.async two tiles ahead, and the tile after that is L2-prefetched;
+//  * phase A (lane = unknown, one warp per t2 slice z of the box): the x (normal) Gram
+//    moments of the slice's <= 7 lines, then the y moments of each distinct t1 window start
+//    s (<= 3), written as T[s][z][pair] to a second shared region;
+//  * phase B (warp = block of the segment's 3 x 3 coarse blocks, lane = unknown): the
+//    block's z moments from its 5 T slices, the synthesis at its <= 27 children, direct
+//    stores (a warp writes contiguous runs of unknowns);
+//  * the two phases run in different warps of one CTA per SM, on consecutive tiles (see
+//    tile3p_interp_kernel below).
 #pragma once
 
 constexpr int T3Y = 7;                    // box extent along t1 / t2 (three 5-cell windows within 7 cells)
@@ -27,7 +24,6 @@ constexpr int T3BOX = 5 * T3Y * T3Y;      // 245 cells: odd pitch, conflict-free
 constexpr int T3TP = 3 * T3Y * 10;        // T region per unknown: [start s][z][pair t]; 210 = 2 mod 16
                                           // doubles: 16-byte accesses of consecutive unknowns are
                                           // conflict-free (pairs of T values per LDS.128 / STS.128)
-constexpr int T3CMAX = 31;                // unknowns per tile (2 CTAs per SM fit in shared memory)
 
 // the normal synthesis table of the operator's single normal group, [child][4], passed as a
 // kernel parameter: the synthesis FMAs take it straight from the constant bank
@@ -56,7 +52,7 @@ __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
 }
 
 // first unknown of chunk c of nch; align: boundaries rounded down to 4 unknowns (32-byte
-// sectors of the AoS cells), chosen by the host when every chunk still fits T3CMAX
+// sectors of the AoS cells) when the host asks for it
 __device__ __forceinline__ int tile3_bound(int c, int nch, int u, int align) {
   if (c >= nch) return u;
   const int b = c * u / nch;
@@ -114,30 +110,6 @@ __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __r
   H.narrow = small(fr.dn) && small(fr.d1) && small(fr.d2) && op.p <= 64 && u <= (1 << 20);
 }
 
-// cp.async copies of the tile's box into box[q][x + 5 (y + T3Y z)]: warps over the box's source
-// lines (y, z) (all 9 warps, so the copies are issued quickly), lanes over the chunk's unknowns
-template <int NTH>
-__device__ __forceinline__ void tile3_fetch(const Tile3Hdr& H, const double* __restrict__ src, double* box,
-                                            int warp = -1) {
-  constexpr int NW = NTH / 32;
-  const int lane = threadIdx.x & 31;
-  if (warp < 0) warp = threadIdx.x >> 5;
-  if (lane >= H.cn) return;
-  const int ny = H.ny, nl = H.ny * H.nz;
-  const unsigned nymag = H.nymag;
-  const int64_t sn = H.sn, s1 = H.s1, s2 = H.s2;
-  const double* const base = src + (H.src_off + lane);
-  double* const bq = box + lane * T3BOX;
-#pragma unroll 1
-  for (int r = warp; r < nl; r += NW) {
-    const int z = int((unsigned(r) * nymag) >> 16), y = r - z * ny;
-    const double* cell = base + (int64_t(y) * s1 + int64_t(z) * s2);
-    double* const drow = bq + 5 * (y + T3Y * z);
-#pragma unroll
-    for (int x = 0; x < 5; ++x, cell += sn) cp_async8(drow + x, cell);
-  }
-}
-
 // L2 prefetch of a tile's box: one source cell per thread, the <= 3 128-byte lines of its chunk
 template <int NTH>
 __device__ __forceinline__ void tile3_prefetch_l2(const Tile3Hdr& H, const double* __restrict__ src, int tid = -1) {
@@ -192,29 +164,6 @@ __device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double
       for (int t = 0; t < 10; t += 2)
         *reinterpret_cast<double2*>(tq + s * (10 * T3Y) + t) = make_double2(T[t], T[t + 1]);
     }
-  }
-}
-
-template <int NTH>
-__device__ __forceinline__ void tile3_phase_a(const Tile3Hdr& H, const double* box, double* tr, double& chk) {
-  // item (z, q) = (warp, lane): conflict-free box / T accesses (odd pitches)
-  const int z = threadIdx.x >> 5;
-  if (z >= H.nz || (threadIdx.x & 31) >= H.cn) return;
-  if (H.ny == 5) tile3_phase_a_ny<5>(H, box, tr, chk, z);
-  else if (H.ny == 6) tile3_phase_a_ny<6>(H, box, tr, chk, z);
-  else if (H.ny == 7) tile3_phase_a_ny<7>(H, box, tr, chk, z);
-}
-
-// phase A by a group of NW warps (warp w of the group takes slices z = w, w + NW, ...)
-template <int NW>
-__device__ __forceinline__ void tile3_phase_a_group(const Tile3Hdr& H, const double* box, double* tr, double& chk,
-                                                    int w) {
-  if ((threadIdx.x & 31) >= H.cn) return;
-#pragma unroll 1
-  for (int z = w; z < H.nz; z += NW) {
-    if (H.ny == 5) tile3_phase_a_ny<5>(H, box, tr, chk, z);
-    else if (H.ny == 6) tile3_phase_a_ny<6>(H, box, tr, chk, z);
-    else if (H.ny == 7) tile3_phase_a_ny<7>(H, box, tr, chk, z);
   }
 }
 
@@ -443,82 +392,53 @@ __device__ __forceinline__ void tile3_phase_b(const Tile3Hdr& H, const DevOp& op
   }
 }
 
-// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (a [G0][12] slot, unused here: the
-// normal table is the kernel parameter syn0) | box[cmax][T3BOX] (+1 to an even count) | T[cmax][T3TP]
-// One CTA per SM (MINB = 1): no spills (126 registers).  Two CTAs per SM need <= 96 registers
-// (<= 5 warps per 16 K-register SM sub-partition) and spill ~200 bytes; on config 5 at full size
-// (196,608 faces over a 52 GB pool) one CTA per SM is 1.30x faster (11.1 vs 14.4 ms, same box,
-// same call; at 24,576 faces two CTAs are 3% faster): profiles/r02_ab_tile3_regs.txt.
-template <int NTH, int MINB>
-__global__ void __launch_bounds__(NTH, MINB)
-    tile3_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
-                        const th_face* __restrict__ faces, int64_t n_tiles, int nt, int nch, int align, int cmax, int u,
-                        int32_t* flag) {
-  static_assert(NTH == 32 * 9, "one warp per block of the 3 x 3 tile (phase B) and per t2 slice (phase A)");
-  extern __shared__ __align__(16) double smem_t3[];
-  __shared__ Tile3Hdr Hs[4];  // tiles it (computing), it + 1 (fetching), it + 2 (L2 prefetch), it + 3 (decoding)
-  const int G1n = op.G1;
-  int4* const sgrp = reinterpret_cast<int4*>(smem_t3);
-  double* const stab = smem_t3 + 2 * G1n;
-  double* const box = smem_t3 + tile_box_offset(12, op.G0, G1n);
-  double* const tr = box + ((cmax * T3BOX + 1) & ~1);  // 16-byte aligned
-  for (int i = threadIdx.x; i < G1n; i += NTH) sgrp[i] = __ldg(&op.grp1[i]);
-  for (int i = threadIdx.x; i < G1n * 12; i += NTH) stab[i] = __ldg(op.synth1 + i);
-  constexpr int DEC = NTH - 1;
-  const int64_t t0 = blockIdx.x, step = gridDim.x;
-  if (threadIdx.x == DEC)
-    for (int i = 0; i < 3; ++i)
-      if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nt, nch, align, u, Hs[i]);
-  __syncthreads();
-  if (t0 < n_tiles) tile3_fetch<NTH>(Hs[0], src, box);
-  cp_async_commit();
-  if (t0 + step < n_tiles) tile3_prefetch_l2<NTH>(Hs[1], src);
-  double chk = 0.0;  // fma(T00, 0, chk) stays 0 for finite inputs, turns NaN for any Inf / NaN
-  int it = 0;
-  for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
-    cp_async_wait_all();
-    __syncthreads();  // this tile's box landed; the previous tile's phase B is done with T
-    const Tile3Hdr& H = Hs[it & 3];
-    tile3_phase_a<NTH>(H, box, tr, chk);
-    __syncthreads();  // T complete, the box is free
-    if (tile + step < n_tiles) tile3_fetch<NTH>(Hs[(it + 1) & 3], src, box);
-    cp_async_commit();
-    // the tile after next into L2, so that its copies above find it there one iteration later
-    if (tile + 2 * step < n_tiles) tile3_prefetch_l2<NTH>(Hs[(it + 2) & 3], src);
-    if (threadIdx.x == DEC && tile + 3 * step < n_tiles)
-      tile3_decode(op, faces, tile + 3 * step, nt, nch, align, u, Hs[(it + 3) & 3]);
-    if (H.narrow) tile3_phase_b<NTH, int>(H, op, dst, tr, stab, syn0, sgrp);
-    else tile3_phase_b<NTH, int64_t>(H, op, dst, tr, stab, syn0, sgrp);
-  }
-  cp_async_wait_all();
-  raise_flag(flag, !isfinite(chk));
-}
-
-
 // ---------------------------------------------------------------------------
-// Warp-specialised variant: phase A and phase B of consecutive tiles run at the same time.
+// The kernel: phase A and phase B of consecutive tiles run at the same time.
 //
-// The two-phase kernel above idles warps at every tile: phase A keeps <= 7 of 9 warps busy
-// and both phases end in a CTA barrier (ncu: barrier the top stall, 2.1 cycles per issue).
+// (Round 1's kernel ran both phases in one group of 9 warps: phase A kept <= 7 of them busy and
+// both phases ended in a CTA barrier -- barrier the top stall, 2.1 cycles per issue; 0.526 of
+// the copy peak on config 5 against 0.60 here, profiles/r02_ab_tile3p.txt.)
 // Here a CTA is NA3 "A" warps + 9 "B" warps.  A warps fetch (cp.async) and project tile i
 // into T[i % 2] while B warps synthesise tile i - 1 from T[(i - 1) % 2]; boxes and T are
-// double-buffered, and the hand-off uses named barriers (bar.arrive by the producer side,
-// bar.sync by the consumer side):
-//   A_BAR (id 1, A warps)       box i landed for every A thread / box i no longer read
-//   T_FULL[b] (ids 2, 3, all)   T[b] written (A arrive, B sync)
-//   T_EMPTY[b] (ids 4, 5, all)  T[b] consumed (B arrive, A sync before rewriting it)
-// A warps also decode the tile headers (ring of 8) and L2-prefetch the tile after next.
-// Same arithmetic as tile3_interp_kernel (results bitwise equal).
+// double-buffered, and the hand-off uses named barriers:
+//   T_FULL[k] (id 1 + k, all)        T[k] written (A arrive, B sync)
+//   T_EMPTY[k] (id 1 + NT + k, all)  T[k] consumed (B arrive, A sync before rewriting it)
+// (mbarrier arrive / try_wait spin hand-offs instead measured 8% slower: the spinning waits
+// take issue slots, profiles/r02_ab_tile3p.txt.)
+// A warp w fetches and projects box slice z = w only (each lane reads only what it copied),
+// so A warps never wait for one another.  They also decode the tile headers (ring of 8) and
+// L2-prefetch the tile after next.
 // ---------------------------------------------------------------------------
-constexpr int NA3 = 4;                 // A warps
+constexpr int NA3 = T3Y;               // A warps: one per t2 slice of the box
 constexpr int T3P_NTH = (NA3 + 9) * 32;
-constexpr int T3PCMAX = 30;            // unknowns per tile: 2 x (box + T) within 227 KB
-
 __device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive_n(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+constexpr int T3PCMAX = 30;            // unknowns per tile: NBOX boxes + NT T buffers within 227 KB
+#ifndef T3P_NBOX
+#define T3P_NBOX 2                     // source boxes (A / B builds: -DT3P_NBOX=1 -DT3P_NT=3)
+#endif
+#ifndef T3P_NT
+#define T3P_NT 2                       // T buffers between the A and B warps
+#endif
+
 __device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// cp.async copies of t2 slice z of a tile's box (all its t1 lines), lanes over the chunk's unknowns
+__device__ __forceinline__ void tile3_fetch_slice(const Tile3Hdr& H, const double* __restrict__ src, double* box, int z) {
+  const int lane = threadIdx.x & 31;
+  if (lane >= H.cn || z >= H.nz) return;
+  const int64_t sn = H.sn, s1 = H.s1;
+  const double* const base = src + (H.src_off + lane + int64_t(z) * H.s2);
+  double* const bq = box + lane * T3BOX + 5 * T3Y * z;
+#pragma unroll 1
+  for (int y = 0; y < H.ny; ++y) {
+    const double* cell = base + int64_t(y) * s1;
+#pragma unroll
+    for (int x = 0; x < 5; ++x, cell += sn) cp_async8(bq + 5 * y + x, cell);
+  }
+}
 
 // dynamic shared memory: sgrp int4[G1] | stab [G1][12] | (unused [G0][12] slot) | box[2][cmax][T3BOX]
 // (each rounded to an even count) | T[2][cmax][T3TP]
@@ -528,49 +448,62 @@ __global__ void __launch_bounds__(T3P_NTH, 1)
                          int u, int32_t* flag) {
   extern __shared__ __align__(16) double smem_t3p[];
   __shared__ Tile3Hdr Hs[8];
+
   const int G1n = op.G1;
   int4* const sgrp = reinterpret_cast<int4*>(smem_t3p);
   double* const stab = smem_t3p + 2 * G1n;
   const int boxd = (cmax * T3BOX + 1) & ~1, trd = cmax * T3TP;
   double* const box0 = smem_t3p + tile_box_offset(12, op.G0, G1n);
-  double* const tr0 = box0 + 2 * boxd;
+  double* const tr0 = box0 + T3P_NBOX * boxd;
   for (int i = threadIdx.x; i < G1n; i += T3P_NTH) sgrp[i] = __ldg(&op.grp1[i]);
   for (int i = threadIdx.x; i < G1n * 12; i += T3P_NTH) stab[i] = __ldg(op.synth1 + i);
   const int warp = threadIdx.x >> 5;
   const int64_t t0 = blockIdx.x, step = gridDim.x;
   constexpr int ALL = T3P_NTH, ANTH = NA3 * 32;
+  constexpr int NBX = T3P_NBOX, NT = T3P_NT;
+  // named barriers: T_FULL[k] = 1 + k, T_EMPTY[k] = 1 + NT + k (bar.arrive by the producing
+  // group, bar.sync by the consuming group; counts include both groups)
+  static_assert(2 * NT + 1 <= 16 && NT + 5 <= 8 + 1, "named barriers / header ring");
   if (warp < NA3) {
     // ============ A warps: fetch, phase A ============
+    // A warp w owns box slice z = w (NA3 == T3Y): it fetches that slice of every tile and takes
+    // the slice's phase A items, each lane only ever reading the cp.async data it copied itself,
+    // so the A warps need no barrier among themselves.
+    static_assert(NA3 == T3Y, "one A warp per t2 slice of the box");
     const int atid = threadIdx.x;
     if (atid == 0)
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 5; ++i)
         if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nt, nch, align, u, Hs[i]);
-    __syncthreads();  // (with the B warps: tables and headers 0..3 visible to everyone)
-    if (t0 < n_tiles) tile3_fetch<ANTH>(Hs[0], src, box0, warp);
-    cp_async_commit();
-    if (t0 + step < n_tiles) tile3_fetch<ANTH>(Hs[1], src, box0 + boxd, warp);
-    cp_async_commit();
-    if (t0 + 2 * step < n_tiles) tile3_prefetch_l2<ANTH>(Hs[2], src, atid);
+    __syncthreads();  // (with the B warps: tables and headers 0..4 visible to everyone)
+    for (int i = 0; i < NBX; ++i) {
+      if (t0 + i * step < n_tiles) tile3_fetch_slice(Hs[i], src, box0 + i * boxd, warp);
+      cp_async_commit();
+    }
+    if (t0 + NBX * step < n_tiles) tile3_prefetch_l2<ANTH>(Hs[NBX], src, atid);
     double chk = 0.0;
     int it = 0;
     for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
-      const int b = it & 1;
-      cp_async_wait_one();
-      bar_sync_n(1, ANTH);                       // box b holds tile `it` for every A thread
-      if (it >= 2) bar_sync_n(4 + b, ALL);       // B is done with T[b] (tile it - 2)
-      if (atid == 0 && tile + 4 * step < n_tiles)  // Hs[(it + 4) & 7]: B is at tile >= it - 1
-        tile3_decode(op, faces, tile + 4 * step, nt, nch, align, u, Hs[(it + 4) & 7]);
+      const int bx = NBX == 1 ? 0 : it % NBX, tb = it % NT;
+      if constexpr (NBX == 1) cp_async_wait_all();   // this thread's slice of tile `it` landed
+      else cp_async_wait_one();
+      if (it >= NT) bar_sync_n(1 + NT + tb, ALL);     // B is done with T[tb] (tile it - NT)
+      if (atid == 0 && tile + 5 * step < n_tiles)     // Hs[(it + 5) & 7]: B is past tile it - NT
+        tile3_decode(op, faces, tile + 5 * step, nt, nch, align, u, Hs[(it + 5) & 7]);
       const Tile3Hdr& H = Hs[it & 7];
-      tile3_phase_a_group<NA3>(H, box0 + b * boxd, tr0 + b * trd, chk, warp);
-      bar_arrive_n(2 + b, ALL);                  // T[b] ready
-      bar_sync_n(1, ANTH);                       // every A thread is done reading box b
-      if (tile + 2 * step < n_tiles) tile3_fetch<ANTH>(Hs[(it + 2) & 7], src, box0 + b * boxd, warp);
+      if (warp < H.nz && (threadIdx.x & 31) < H.cn) {
+        double* const bxp = box0 + bx * boxd;
+        if (H.ny == 5) tile3_phase_a_ny<5>(H, bxp, tr0 + tb * trd, chk, warp);
+        else if (H.ny == 6) tile3_phase_a_ny<6>(H, bxp, tr0 + tb * trd, chk, warp);
+        else if (H.ny == 7) tile3_phase_a_ny<7>(H, bxp, tr0 + tb * trd, chk, warp);
+      }
+      bar_arrive_n(1 + tb, ALL);                      // T[tb] ready (once every A thread arrived)
+      if (tile + NBX * step < n_tiles) tile3_fetch_slice(Hs[(it + NBX) & 7], src, box0 + bx * boxd, warp);
       cp_async_commit();
-      if (tile + 3 * step < n_tiles) tile3_prefetch_l2<ANTH>(Hs[(it + 3) & 7], src, atid);
+      if (tile + (NBX + 1) * step < n_tiles) tile3_prefetch_l2<ANTH>(Hs[(it + NBX + 1) & 7], src, atid);
     }
-    // drain: the B warps' T_EMPTY arrivals of the last two tiles have no matching sync yet
-    for (int k = it - 2; k < it; ++k)
-      if (k >= 0) bar_sync_n(4 + (k & 1), ALL);
+    // drain: the B warps' T_EMPTY arrivals of the last NT tiles have no matching sync yet
+    for (int k = it - NT; k < it; ++k)
+      if (k >= 0) bar_sync_n(1 + NT + k % NT, ALL);
     cp_async_wait_all();
     raise_flag(flag, !isfinite(chk));
   } else {
@@ -578,13 +511,13 @@ __global__ void __launch_bounds__(T3P_NTH, 1)
     __syncthreads();
     int it = 0;
     for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
-      const int b = it & 1;
-      bar_sync_n(2 + b, ALL);                    // T[b] holds tile `it`
+      const int tb = it % NT;
+      bar_sync_n(1 + tb, ALL);                   // T[tb] holds tile `it`
       const Tile3Hdr& H = Hs[it & 7];
       // phase B with the B warps renumbered 0..8 (tile3_phase_b maps warp -> block)
-      if (H.narrow) tile3_phase_b<T3P_NTH, int>(H, op, dst, tr0 + b * trd, stab, syn0, sgrp, warp - NA3);
-      else tile3_phase_b<T3P_NTH, int64_t>(H, op, dst, tr0 + b * trd, stab, syn0, sgrp, warp - NA3);
-      bar_arrive_n(4 + b, ALL);                  // T[b] consumed
+      if (H.narrow) tile3_phase_b<T3P_NTH, int>(H, op, dst, tr0 + tb * trd, stab, syn0, sgrp, warp - NA3);
+      else tile3_phase_b<T3P_NTH, int64_t>(H, op, dst, tr0 + tb * trd, stab, syn0, sgrp, warp - NA3);
+      bar_arrive_n(1 + NT + tb, ALL);            // T[tb] consumed
     }
   }
 }

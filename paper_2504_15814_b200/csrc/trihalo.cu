@@ -925,14 +925,12 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     }
   }
   static const int use_tile3 = [] { const char* e = std::getenv("TH_TILE3"); return e ? std::atoi(e) : 1; }();
-  //   TH_TILE3P=1               warp-specialised order3 tiles (phase A / B of consecutive tiles overlap)
-  static const int use_tile3p = [] { const char* e = std::getenv("TH_TILE3P"); return e ? std::atoi(e) : 0; }();
-  if (use_tile3 && use_tile3p && interp && op->t3_ok && op->t3_nt == 1) {
+  if (use_tile3 && interp && op->t3_ok && op->t3_nt == 1) {
     const int nch = (u + T3PCMAX - 1) / T3PCMAX;
     int cmax = 0;
     for (int c = 0; c < nch; ++c) cmax = std::max(cmax, (c + 1) * u / nch - c * u / nch);
     const size_t smem = 8 * (size_t(tile_box_offset(12, op->dev.G0, op->dev.G1)) +
-                             2 * size_t((cmax * T3BOX + 1) & ~1) + 2 * size_t(cmax) * T3TP);
+                             T3P_NBOX * size_t((cmax * T3BOX + 1) & ~1) + T3P_NT * size_t(cmax) * T3TP);
     if (smem <= 227 * 1024) {
       auto kfn = tile3p_interp_kernel;
       int per_sm = 0;
@@ -942,35 +940,6 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       T3Syn0 syn0;
       std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
       kfn<<<tblocks, T3P_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, 1, nch, 0, cmax, u, flag);
-      TH_CUDA(cudaGetLastError());
-      return TH_OK;
-    }
-  }
-  if (use_tile3 && interp && op->t3_ok && op->t3_nt == 1) {
-    // tiles = (face, chunk of <= T3CMAX unknowns); chunk boundaries on 4-unknown (32-byte)
-    // sector edges when every chunk still fits
-    const int nch = (u + T3CMAX - 1) / T3CMAX;
-    int align = 1, cmax = 0;
-    for (int c = 0; c < nch; ++c) {
-      const int b0 = (c * u / nch) & ~3, b1 = c + 1 < nch ? ((c + 1) * u / nch) & ~3 : u;
-      if (b1 - b0 > T3CMAX || b1 <= b0) align = 0;
-    }
-    for (int c = 0; c < nch; ++c) {
-      int b0 = c * u / nch, b1 = (c + 1) * u / nch;
-      if (align) b0 &= ~3, b1 = c + 1 < nch ? b1 & ~3 : u;
-      cmax = std::max(cmax, b1 - b0);
-    }
-    const size_t smem = 8 * (size_t(tile_box_offset(12, op->dev.G0, op->dev.G1)) + size_t((cmax * T3BOX + 1) & ~1) + size_t(cmax) * T3TP);
-    const int nt = op->t3_nt;
-    const int64_t tiles = n_faces * int64_t(nt * nt * nch);
-    if (smem <= 227 * 1024) {
-      auto kfn = tile3_interp_kernel<288, 1>;
-      int per_sm = 0;
-      TH_CUDA(resident_ctas(reinterpret_cast<const void*>(kfn), 288, smem, &per_sm));
-      const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));
-      T3Syn0 syn0;
-      std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
-      kfn<<<tblocks, 288, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, nt, nch, align, cmax, u, flag);
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }

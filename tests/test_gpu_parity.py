@@ -355,13 +355,13 @@ def test_pool_transposed_layout(th, scheme, p):
 
 
 @pytest.mark.parametrize("env", ({"TH_GRAM": "3"}, {"TH_TILE": "0"}, {"TH_TILE3": "0"},
-                                 {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_TILE3P": "1"}))
+                                 {"TH_TILE": "0", "TH_GRAM": "0"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
     parity tests in a child process with the alternative paths (the per-warp order3
     restriction slide; the per-warp interpolation slide instead of the staged tile kernel;
     the per-warp slide for order3 interpolation instead of the two-phase order3 tiles; the
-    fixed-window kernels with neither tiles nor Gram slides; the warp-specialised order3 tiles)."""
+    fixed-window kernels with neither tiles nor Gram slides)."""
     import os
     import subprocess
     import sys
