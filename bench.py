@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--fine-layout", choices=("random", "siblings"), default="random",
+                    help="config 5 diagnosis: the nine fine patches of a face uniform over the pool (default) "
+                         "or consecutive ids")
     ap.add_argument("--straddle", type=float, default=0.0,
                     help="config 5: fraction of faces with one fine patch drawn from the whole pool (A/B, tests)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink patch / face counts (tuning runs only)")
@@ -513,14 +516,15 @@ def run_multi(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     t_setup = time.perf_counter()
-    wl = W.describe_multi(world, scale=args.scale, straddle=args.straddle)
+    wl = W.describe_multi(world, scale=args.scale, straddle=args.straddle, fine_layout=args.fine_layout)
     s = wl.spec
     p, k, u = s.p, s.k, s.u
     ops = {role: th.operators.DEFAULT_CACHE.device_operator(role, "order3", p, k)
            for role in ("interpolate", "restrict")}
     support = Support.from_operators(ops["interpolate"], ops["restrict"], p, k)
     plan = plan_sweep(wl.part, wl.coarse, wl.fine, wl.segment, rank, wl.normal, wl.side, support=support)
-    wl = W.build_multi(world, rank, scale=args.scale, src_elems=plan.src_elems(p, k, u), straddle=args.straddle)
+    wl = W.build_multi(world, rank, scale=args.scale, src_elems=plan.src_elems(p, k, u), straddle=args.straddle,
+                       fine_layout=args.fine_layout)
     lo = int(wl.part.bounds[rank])
     per = k * p * p * u
     if world > 1:
@@ -589,7 +593,8 @@ def run_multi(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: cubic polynomial field per unknown + 1e-6 N(0,1) noise, generated in HBM (seeded per "
                 "64-patch group, partition-independent); fine patches drawn from the pool by index lists",
-        "config": c5_config(s, world, args.straddle),
+        "config": {**c5_config(s, world, args.straddle),
+                   **({"fine_layout": args.fine_layout} if args.fine_layout != "random" else {})},
         "roofline": {"bound": "hbm", "kernel": f"{rows[dom]['role']}:order3 ({rows[dom]['kind']} faces)",
                      "achieved": rows[dom]["alg_GBps"], "peak": peak, "unit": "GB/s", "frac": rows[dom]["frac_hbm"],
                      "frac_8tbs": rows[dom]["frac_8tbs"], "traffic": None,

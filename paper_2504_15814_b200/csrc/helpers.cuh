@@ -33,12 +33,23 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+#ifndef TH_MBAR_HINT
+#define TH_MBAR_HINT 0  // suspend-time hint (ns) of the try_wait loop; 0: none (A/B builds: -DTH_MBAR_HINT=n)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+#if TH_MBAR_HINT > 0
+  asm volatile(
+      "{ .reg .pred P; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2; @!P bra WAIT_%=; }" ::"r"(
+          smem_u32(b)),
+      "r"(parity), "n"(TH_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{ .reg .pred P; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1; @!P bra WAIT_%=; }" ::"r"(
           smem_u32(b)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");

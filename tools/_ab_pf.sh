@@ -1,0 +1,6 @@
+TH_LIBPATH=$PWD/_lib_ab/pf6/libtrihalo_b200.so timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "restrict" 2>&1 | tail -1
+for v in base pf3 pf6 pf10 base pf3 pf6 pf10; do
+  if [ $v = base ]; then unset TH_LIBPATH; else export TH_LIBPATH=$PWD/_lib_ab/$v/libtrihalo_b200.so; fi
+  timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/abf_$v.json 2>/dev/null; echo "c5 $v"; python tools/bench_brief.py gpurun_out/abf_$v.json | sed -n 1,2p
+  timeout 600 python bench.py --scale 0.125 --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/abf8_$v.json 2>/dev/null; echo "c5/8 $v"; python tools/bench_brief.py gpurun_out/abf8_$v.json | sed -n 2,2p
+done

@@ -346,7 +346,8 @@ class MultiWorkload:
     src: object = None        # source tensor: pool + staging slots + received boxes
 
 
-def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10, straddle: float = 0.0) -> MultiWorkload:
+def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10, straddle: float = 0.0,
+                   fine_layout: str = "random") -> MultiWorkload:
     """Global face list of config 5 (identical on every rank).
 
     BASELINE: 10% of faces have coarse and fine patches on different GPUs, the partner GPU
@@ -374,6 +375,9 @@ def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10, straddle
     lo = part.bounds[f_own]
     size = part.bounds[f_own + 1] - lo
     fine = lo[:, None] + (rng.random((nf, 9)) * size[:, None]).astype(np.int64)
+    if fine_layout == "siblings":  # diagnosis only: the nine fine patches are consecutive ids
+        base = lo + (rng.random(nf) * np.maximum(size - 9, 1)).astype(np.int64)
+        fine = base[:, None] + np.arange(9)[None, :]
     if straddle > 0:
         srng = np.random.default_rng(spec.seed + 17)
         st = srng.random(nf) < straddle
@@ -430,12 +434,12 @@ def patch_values(wl: MultiWorkload, ids, device="cuda"):
 
 
 def build_multi(world: int, rank: int, scale: float = 1.0, src_elems: int | None = None,
-                straddle: float = 0.0) -> MultiWorkload:
+                straddle: float = 0.0, fine_layout: str = "random") -> MultiWorkload:
     """Config 5 on this rank: its pool (patches [lo, hi)) at the front of a source tensor of
     `src_elems` elements (multigpu.SweepPlan.src_elems: pool + staging + received boxes)."""
     import torch
 
-    wl = describe_multi(world, scale, straddle=straddle)
+    wl = describe_multi(world, scale, straddle=straddle, fine_layout=fine_layout)
     s = wl.spec
     E = s.p + 2 * s.k
     lo, hi = int(wl.part.bounds[rank]), int(wl.part.bounds[rank + 1])
