@@ -210,6 +210,23 @@ int32_t th_pseudoinverse_rows(const double* a, int32_t s, int32_t n, double* w, 
  * HBM for callers that hold their data on the host. */
 int32_t th_memcpy_async(void* dst, const void* src, int64_t bytes, int32_t kind, void* stream);
 
+/* Copy the same set of blocks out of n_patches consecutive patches (host <-> device, kind as
+ * th_memcpy_async): a patch is patch_elems doubles, seen as rows of row_elems doubles; block b
+ * = blocks[4b .. 4b+3] = {first row, rows, first element in the row, elements per row}.  One
+ * cudaMemcpy3DAsync per block (rows x patches).  Ships only the cells a sweep reads from a
+ * patch pool held in host memory. */
+int32_t th_copy_patch_blocks(void* dst, const void* src, int64_t n_patches, int64_t patch_elems, int64_t row_elems,
+                             const int32_t* blocks, int32_t n_blocks, int32_t kind, void* stream);
+
+/* Pack (pack = 1: pool -> compact) or unpack (0: compact -> pool) the same blocks of n_patches
+ * consecutive patches, all device memory.  blocks (device, int32 [n_blocks][4], the format of
+ * th_copy_patch_blocks); block_offsets (device, int64 [n_blocks]) = each block's element offset
+ * inside a patch's compact record of compact_elems elements.  Lets a host hold only the cells a
+ * sweep reads, contiguously, and ship them with plain copies. */
+int32_t th_pool_blocks(double* pool, double* compact, int64_t n_patches, int64_t patch_elems, int64_t row_elems,
+                       const int32_t* blocks, const int64_t* block_offsets, int32_t n_blocks, int64_t compact_elems,
+                       int32_t pack, void* stream);
+
 /* Copy n_boxes cell boxes (th_box records in DEVICE memory) from src to dst, both
  * device.  Boxes must not overlap one another's targets, nor a target overlap a
  * source of the same launch.  Bit-exact. */

@@ -71,6 +71,7 @@ EXPORTED = (
     "th_operator_destroy", "th_operator_info_get", "th_operator_export_rows", "th_apply_faces",
     "th_check_finite", "th_csr_apply", "th_operator_support_layers", "th_copy_box_layers", "th_copy_faces",
     "th_copy_boxes", "th_operator_source_box", "th_memcpy_async", "th_pseudoinverse_rows",
+    "th_copy_patch_blocks", "th_pool_blocks",
 )
 
 _lib = None
@@ -126,6 +127,10 @@ def load():
     lib.th_memcpy_async.argtypes = [_vp, _vp, _i64, _i32, _vp]
     lib.th_pseudoinverse_rows.restype = _i32
     lib.th_pseudoinverse_rows.argtypes = [_vp, _i32, _i32, _vp, ctypes.POINTER(ctypes.c_double)]
+    lib.th_copy_patch_blocks.restype = _i32
+    lib.th_copy_patch_blocks.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _i32, _vp]
+    lib.th_pool_blocks.restype = _i32
+    lib.th_pool_blocks.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _i32, _vp]
     lib.th_csr_apply.restype = _i32
     lib.th_csr_apply.argtypes = [_vp, _vp, _vp, _i64, _vp, _vp, _i32, _vp]
     _lib = lib

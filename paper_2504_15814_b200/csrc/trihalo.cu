@@ -926,7 +926,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     }
   }
   static const int use_tile3 = [] { const char* e = std::getenv("TH_TILE3"); return e ? std::atoi(e) : 1; }();
-  if (use_tile3 && interp && op->t3_ok && op->t3_nt == 1) {
+  //   TH_TILE3=2                 also when a face splits into several spatial tiles (p = 17)
+  if (use_tile3 && interp && op->t3_ok && (op->t3_nt == 1 || use_tile3 == 2)) {
     const int nch = (u + T3PCMAX - 1) / T3PCMAX;
     int cmax = 0;
     for (int c = 0; c < nch; ++c) cmax = std::max(cmax, (c + 1) * u / nch - c * u / nch);
@@ -936,11 +937,12 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       auto kfn = tile3p_interp_kernel;
       int per_sm = 0;
       TH_CUDA(resident_ctas(reinterpret_cast<const void*>(kfn), T3P_NTH, smem, &per_sm));
-      const int64_t tiles = n_faces * int64_t(nch);
+      const int nt = op->t3_nt;
+      const int64_t tiles = n_faces * int64_t(nt * nt * nch);
       const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1)));
       T3Syn0 syn0;
       std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
-      kfn<<<tblocks, T3P_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, 1, nch, 0, cmax, u, flag);
+      kfn<<<tblocks, T3P_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, nt, nch, 0, cmax, u, flag);
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
@@ -1183,6 +1185,69 @@ int32_t th_pseudoinverse_rows(const double* a, int32_t s, int32_t n, double* w, 
   } catch (const th::Error& e) {
     return fail(map_error(e), e.what(), e.column);
   }
+  return TH_OK;
+}
+
+int32_t th_copy_patch_blocks(void* dst, const void* src, int64_t n_patches, int64_t patch_elems, int64_t row_elems,
+                             const int32_t* blocks, int32_t n_blocks, int32_t kind, void* stream) {
+  if (n_patches <= 0 || n_blocks <= 0) return TH_OK;
+  if (!dst || !src || !blocks) return fail(TH_ERR_CONTRACT, "NULL pointer");
+  if (patch_elems <= 0 || row_elems <= 0 || patch_elems % row_elems)
+    return fail(TH_ERR_CONFIG, "patch_elems must be a positive multiple of row_elems");
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  const size_t pitch = size_t(row_elems) * 8, rows_per_patch = size_t(patch_elems / row_elems);
+  for (int b = 0; b < n_blocks; ++b) {
+    const int32_t row0 = blocks[4 * b], nrows = blocks[4 * b + 1], x0 = blocks[4 * b + 2], w = blocks[4 * b + 3];
+    if (row0 < 0 || nrows <= 0 || x0 < 0 || w <= 0 || x0 + w > row_elems || size_t(row0 + nrows) > rows_per_patch)
+      return fail(TH_ERR_CONFIG, "block outside the patch");
+    cudaMemcpy3DParms prm;
+    std::memset(&prm, 0, sizeof(prm));
+    prm.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), pitch, pitch, rows_per_patch);
+    prm.dstPtr = make_cudaPitchedPtr(dst, pitch, pitch, rows_per_patch);
+    prm.srcPos = make_cudaPos(size_t(x0) * 8, size_t(row0), 0);
+    prm.dstPos = prm.srcPos;
+    prm.extent = make_cudaExtent(size_t(w) * 8, size_t(nrows), size_t(n_patches));
+    prm.kind = k;
+    TH_CUDA(cudaMemcpy3DAsync(&prm, static_cast<cudaStream_t>(stream)));
+  }
+  return TH_OK;
+}
+
+// Pack / unpack the same blocks of every patch between a patch pool and a compact layout
+// (per patch: the blocks back to back, each rows x width elements).  Warp per (patch, block).
+__global__ void __launch_bounds__(256) patch_blocks_kernel(double* __restrict__ pool, double* __restrict__ compact,
+                                                           int64_t n_patches, int64_t patch_elems, int64_t row_elems,
+                                                           const int4* __restrict__ blocks, const int64_t* __restrict__ boff,
+                                                           int n_blocks, int64_t compact_elems, int pack) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t units = n_patches * n_blocks;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < units; w += nw) {
+    const int64_t pt = w / n_blocks;
+    const int b = int(w - pt * n_blocks);
+    const int4 B = __ldg(&blocks[b]);  // (row0, rows, x0, width)
+    double* const pp = pool + pt * patch_elems + int64_t(B.x) * row_elems + B.z;
+    double* const cp = compact + pt * compact_elems + __ldg(&boff[b]);
+    const int n = B.y * B.w;
+    for (int e = lane; e < n; e += 32) {
+      const int r = e / B.w, c = e - r * B.w;
+      if (pack) cp[e] = pp[int64_t(r) * row_elems + c];
+      else pp[int64_t(r) * row_elems + c] = cp[e];
+    }
+  }
+}
+
+int32_t th_pool_blocks(double* pool, double* compact, int64_t n_patches, int64_t patch_elems, int64_t row_elems,
+                       const int32_t* blocks, const int64_t* block_offsets, int32_t n_blocks, int64_t compact_elems,
+                       int32_t pack, void* stream) {
+  if (n_patches <= 0 || n_blocks <= 0) return TH_OK;
+  if (!pool || !compact || !blocks || !block_offsets) return fail(TH_ERR_CONTRACT, "NULL pointer");
+  const int64_t units = n_patches * n_blocks;
+  const int grid = int(std::min<int64_t>((units + 7) / 8, int64_t(num_sms()) * 8));
+  patch_blocks_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      pool, compact, n_patches, patch_elems, row_elems, reinterpret_cast<const int4*>(blocks), block_offsets, n_blocks,
+      compact_elems, pack);
+  TH_CUDA(cudaGetLastError());
   return TH_OK;
 }
 

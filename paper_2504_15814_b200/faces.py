@@ -170,6 +170,45 @@ def pool_restrict_faces(p: int, k: int, u: int, fine_ids, normals, sides, half=N
     return rec
 
 
+def pool_face_blocks(p: int, k: int, u: int) -> np.ndarray:
+    """The cells of a halo-padded patch that 3:1 face work can read, as copy blocks.
+
+    Interpolation reads the coarse patch's normal layers [p, p + 2k) or [0, 2k) by [k, k + p)
+    tangentially; restriction reads the same layers of each fine patch.  The union
+    over the six faces (2,160 of 3,375 cells at p = 9, k = 3) is returned as blocks
+    {first row, rows, first element, elements} with a row = one x-line of E cells (E u
+    elements) and row index z E + y -- the format of th_copy_patch_blocks."""
+    E = p + 2 * k
+    need = np.zeros((E, E, E), dtype=bool)  # [z][y][x]
+    t = slice(k, k + p)
+    for n in range(3):
+        for lo in (0, p):
+            sl = [t, t, t]
+            sl[2 - n] = slice(lo, lo + 2 * k)
+            need[tuple(sl)] = True
+    runs = {}
+    for z in range(E):
+        for y in range(E):
+            x = 0
+            while x < E:
+                if need[z, y, x]:
+                    s0 = x
+                    while x < E and need[z, y, x]:
+                        x += 1
+                    runs.setdefault((z, s0, x - s0), []).append(y)
+                else:
+                    x += 1
+    blocks = []
+    for (z, x0, n), ys in sorted(runs.items()):
+        start = prev = ys[0]
+        for y in ys[1:] + [None]:
+            if y is None or y != prev + 1:
+                blocks.append((z * E + start, prev - start + 1, x0 * u, n * u))
+                start = y
+            prev = y if y is not None else prev
+    return np.array(blocks, dtype=np.int32)
+
+
 def pool_same_level_faces(p: int, k: int, u: int, src_ids, dst_ids, normals, sides) -> np.ndarray:
     """Same-level halo faces of the patch pool.
 
