@@ -633,7 +633,7 @@ def run_multi(args, rank, world, local_rank):
     return res
 
 
-def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world, n_chunks=16):
+def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world):
     """Config 5 end to end through the C ABI with HOST buffers.
 
     The host holds this rank's patch pool compactly: per patch only the cells face work reads
@@ -645,6 +645,26 @@ def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world, n_chun
     arrived (faces ordered by their largest fine patch id), and read those results back into
     page-locked host memory (th_memcpy_async) -- upload, kernels and read-back overlap on three
     streams.  Faces that cross ranks (N > 1) go through the sweep's exchange after the upload."""
+    import torch
+
+    try:
+        st = _c5_e2e_setup(wl, plan, sweep, ops, p, k, u, lo, dev)
+        err = None
+    except Exception as exc:  # noqa: BLE001 -- reported in the JSON line
+        st, err = None, f"{type(exc).__name__}: {exc}"
+    if world > 1:  # every rank set up, or none runs the leg (no rank left waiting in a collective)
+        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        if float(ok.item()) < 1.0 and err is None:
+            err = "another rank could not set up the e2e leg"
+    if err:
+        if st is not None:
+            st["release"]()
+        return {"error": err}
+    return _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st)
+
+
+def _c5_e2e_setup(wl, plan, sweep, ops, p, k, u, lo, dev, n_chunks=16):
     import torch
 
     import paper_2504_15814_b200 as th
@@ -707,6 +727,27 @@ def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world, n_chun
         rec = th.pool_restrict_faces(p, k, u, wl.fine[ids] - lo, wl.normal[ids], wl.side[ids],
                                      dst_offsets=np.arange(a, b, dtype=np.int64) * per) if b > a else None
         chunk_r.append((th.FaceBatch(ops["restrict"], rec, u) if rec is not None else None, a, b))
+
+    def release():
+        for a in registered:
+            reg.cudaHostUnregister(a.ctypes.data)
+
+    return dict(lib=lib, pool=pool, E=E, patch=patch, per=per, n_local=n_local, blocks=blocks, d_blocks=d_blocks,
+                d_boff=d_boff, ce=ce, cb=cb, staging=staging, rp_i=rp_i, rp_r=rp_r, nr=nr, rout=rout,
+                host_compact=host_compact, host_i=host_i, host_r=host_r, chunk_i=chunk_i, chunk_r=chunk_r,
+                order=order, n_chunks=n_chunks, release=release)
+
+
+def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
+    import torch
+
+    from paper_2504_15814_b200 import _native
+
+    lib, pool, E, patch, per, n_local = st["lib"], st["pool"], st["E"], st["patch"], st["per"], st["n_local"]
+    blocks, d_blocks, d_boff, ce, cb = st["blocks"], st["d_blocks"], st["d_boff"], st["ce"], st["cb"]
+    staging, rp_i, rp_r, nr, rout = st["staging"], st["rp_i"], st["rp_r"], st["nr"], st["rout"]
+    host_compact, host_i, host_r = st["host_compact"], st["host_i"], st["host_r"]
+    chunk_i, chunk_r, order, n_chunks = st["chunk_i"], st["chunk_r"], st["order"], st["n_chunks"]
     s_in, s_run, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
     def d2h(host, dev_buf, a, b):
@@ -780,9 +821,7 @@ def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world, n_chun
         if nr:
             slot = int(order[j])  # e2e position j holds local restriction face order[j]
             agree &= bool(np.array_equal(host_r[j * per:(j + 1) * per], orr[slot * per:(slot + 1) * per].cpu().numpy()))
-    for a in registered:
-        reg.cudaHostUnregister(a.ctypes.data)
-    del staging, rout
+    st["release"]()
     values = 2 * wl.spec.n_faces * per
     return {"value": values / t_step, "unit": "values/s",
             "h2d_bytes_per_step": int(n_local * ce * 8),
