@@ -129,3 +129,83 @@ def test_empty_batch_and_nonfinite_flag(env):
     batch.launch(src, out)
     assert batch.nonfinite()
     assert not batch.nonfinite()  # read-and-clear
+
+
+def test_pool_offsets_beyond_2_31_elements(env):
+    """Config-5-sized element offsets: a pool of 11,000 patches (2.19e9 elements, 17.5 GB)
+    whose faces read patches past element 2^31 -- every scheme, both roles, against the oracle,
+    and the same-level copy bit for bit (64-bit offsets in every kernel)."""
+    th, torch = env
+    from oracle import exchange as OE
+    from oracle import geometry as OG
+
+    p, k, u = 9, 3, 59
+    E = p + 2 * k
+    patch = E ** 3 * u
+    n_patch = 11000
+    assert n_patch * patch > 2 ** 31
+    dev = torch.device("cuda")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 24 * 2 ** 30:
+        pytest.skip("needs ~24 GB of free device memory")
+    pool = torch.empty(n_patch * patch, dtype=torch.float64, device=dev)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    for a in range(0, n_patch, 1000):  # fill in slices (randn of 2e9 values at once needs 2x)
+        b = min(n_patch, a + 1000)
+        pool[a * patch:b * patch] = torch.randn((b - a) * patch, dtype=torch.float64, device=dev, generator=gen)
+    rng = np.random.default_rng(4)
+    hi = 2 ** 31 // patch + 1  # first patch entirely past element 2^31
+    n_face = 24
+    cid = rng.integers(hi, n_patch, n_face)
+    nrm, sid, seg = rng.integers(0, 3, n_face), rng.integers(0, 2, n_face), rng.integers(0, 9, n_face)
+    fine = rng.integers(hi, n_patch, (n_face, 9))
+    need = np.unique(np.concatenate([cid, fine.ravel()]))
+    host = {int(g): pool[g * patch:(g + 1) * patch].cpu().numpy().reshape(E, E, E, u) for g in need}
+    per = k * p * p * u
+    for scheme in ("tensor_linear", "matrix_linear", "order2", "order3"):
+        for role in ("interpolate", "restrict"):
+            rec = (th.pool_interp_faces(p, k, u, cid, nrm, sid, seg) if role == "interpolate"
+                   else th.pool_restrict_faces(p, k, u, fine, nrm, sid))
+            op = th.operators.DEFAULT_CACHE.device_operator(role, scheme, p, k)
+            out = torch.empty(n_face * per, dtype=torch.float64, device=dev)
+            th.FaceBatch(op, rec, u).launch(pool, out)
+            got = out.cpu().numpy().reshape(n_face, per)
+            for f in range(0, n_face, 3):
+                n, sd = int(nrm[f]), int(sid[f])
+                t1, t2 = [d for d in range(3) if d != n]
+                if role == "interpolate":
+                    lo, ext = [k, k, k], [p, p, p]
+                    lo[n], ext[n] = (p if sd == 0 else 0), 2 * k
+                    src = host[int(cid[f])][lo[2]:lo[2] + ext[2], lo[1]:lo[1] + ext[1], lo[0]:lo[0] + ext[0]]
+                    src, s = src.reshape(-1), int(seg[f])
+                else:
+                    ext = [3 * p, 3 * p, 3 * p]
+                    ext[n] = 2 * k
+                    box = np.zeros((ext[2], ext[1], ext[0], u))
+                    for bb in range(9):
+                        lo, e = [k, k, k], [p, p, p]
+                        lo[n], e[n] = (0 if sd == 0 else p), 2 * k
+                        off = [0, 0, 0]
+                        off[t1], off[t2] = (bb % 3) * p, (bb // 3) * p
+                        box[off[2]:off[2] + e[2], off[1]:off[1] + e[1], off[0]:off[0] + e[0]] = \
+                            host[int(fine[f, bb])][lo[2]:lo[2] + e[2], lo[1]:lo[1] + e[1], lo[0]:lo[0] + e[0]]
+                    src, s = box.reshape(-1), 0
+                ex = OE.exchange_for(OG.FaceCfg("xyz"[n], ("negative", "positive")[sd], s, p, k, u), scheme, role)
+                want = np.empty(ex.n_out)
+                ex.run(src, want)
+                assert np.abs(got[f] - want).max() / np.abs(want).max() <= 1e-12, (scheme, role, f)
+    # same-level halo copy between patches past 2^31
+    src_ids, dst_ids = fine[:4, 0], fine[:4, 1]
+    rec = th.pool_same_level_faces(p, k, u, src_ids, dst_ids, nrm[:4], sid[:4])
+    if len(set(dst_ids.tolist())) == 4 and not set(src_ids.tolist()) & set(dst_ids.tolist()):
+        th.copy_faces(pool, pool, rec, k, p, u)
+        v = pool.view(n_patch, E, E, E, u)
+        for i in range(4):
+            ax = 2 - int(nrm[i])
+            a = [slice(k, k + p)] * 3
+            b = list(a)
+            a[ax] = slice(p, p + k) if sid[i] == 0 else slice(k, 2 * k)
+            b[ax] = slice(0, k) if sid[i] == 0 else slice(p + k, p + 2 * k)
+            assert torch.equal(v[(int(src_ids[i]), *a)], v[(int(dst_ids[i]), *b)])
+    del pool
+    torch.cuda.empty_cache()
