@@ -926,8 +926,9 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     }
   }
   static const int use_tile3 = [] { const char* e = std::getenv("TH_TILE3"); return e ? std::atoi(e) : 1; }();
-  //   TH_TILE3=2                 also when a face splits into several spatial tiles (p = 17)
-  if (use_tile3 && interp && op->t3_ok && (op->t3_nt == 1 || use_tile3 == 2)) {
+  // one spatial tile per face only: at p = 17 (3 x 3 tiles per face, overlapping boxes) the
+  // warp-specialised tiles run 0.27 of the copy peak against the per-warp slide's 0.40
+  if (use_tile3 && interp && op->t3_ok && op->t3_nt == 1) {
     const int nch = (u + T3PCMAX - 1) / T3PCMAX;
     int cmax = 0;
     for (int c = 0; c < nch; ++c) cmax = std::max(cmax, (c + 1) * u / nch - c * u / nch);
