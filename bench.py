@@ -648,7 +648,7 @@ def run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world):
     import torch
 
     try:
-        st = _c5_e2e_setup(wl, plan, sweep, ops, p, k, u, lo, dev)
+        st = _c5_e2e_setup(wl, plan, sweep, ops, p, k, u, lo, dev, n_chunks=args.e2e_chunks)
         err = None
     except Exception as exc:  # noqa: BLE001 -- reported in the JSON line
         st, err = None, f"{type(exc).__name__}: {exc}"
