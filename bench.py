@@ -691,9 +691,10 @@ def _c5_e2e_setup(wl, plan, sweep, ops, p, k, u, lo, dev, n_chunks=16):
     host_compact = np.empty(max(1, n_local * ce), dtype=np.float64)
     host_i = np.empty(max(1, rp_i.n_out * per), dtype=np.float64)
     host_r = np.empty(max(1, nr * per), dtype=np.float64)
+    host_rx = np.empty(max(1, (rp_r.n_out - nr) * per), dtype=np.float64)  # staged + received (N > 1)
     reg = torch._C._cudart
     registered = []
-    for a in (host_compact, host_i, host_r):
+    for a in (host_compact, host_i, host_r, host_rx):
         rc = reg.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
         if int(rc) != 0:
             raise RuntimeError(f"cudaHostRegister failed: {rc}")
@@ -734,7 +735,8 @@ def _c5_e2e_setup(wl, plan, sweep, ops, p, k, u, lo, dev, n_chunks=16):
 
     return dict(lib=lib, pool=pool, E=E, patch=patch, per=per, n_local=n_local, blocks=blocks, d_blocks=d_blocks,
                 d_boff=d_boff, ce=ce, cb=cb, staging=staging, rp_i=rp_i, rp_r=rp_r, nr=nr, rout=rout,
-                host_compact=host_compact, host_i=host_i, host_r=host_r, chunk_i=chunk_i, chunk_r=chunk_r,
+                host_compact=host_compact, host_i=host_i, host_r=host_r, host_rx=host_rx, chunk_i=chunk_i,
+                chunk_r=chunk_r,
                 order=order, n_chunks=n_chunks, release=release)
 
 
@@ -746,7 +748,7 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
     lib, pool, E, patch, per, n_local = st["lib"], st["pool"], st["E"], st["patch"], st["per"], st["n_local"]
     blocks, d_blocks, d_boff, ce, cb = st["blocks"], st["d_blocks"], st["d_boff"], st["ce"], st["cb"]
     staging, rp_i, rp_r, nr, rout = st["staging"], st["rp_i"], st["rp_r"], st["nr"], st["rout"]
-    host_compact, host_i, host_r = st["host_compact"], st["host_i"], st["host_r"]
+    host_compact, host_i, host_r, host_rx = st["host_compact"], st["host_i"], st["host_r"], st["host_rx"]
     chunk_i, chunk_r, order, n_chunks = st["chunk_i"], st["chunk_r"], st["order"], st["n_chunks"]
     s_in, s_run, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
@@ -793,6 +795,9 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
             sweep.post(comp)
             run_done()
         d2h(host_i, sweep.out["interpolate"], rp_i.local.size, rp_i.n_out)
+        if rp_r.n_out > nr:
+            _native.check(lib.th_memcpy_async(host_rx.ctypes.data, sweep.out["restrict"][nr * per:].data_ptr(),
+                                              (rp_r.n_out - nr) * per * 8, 1, s_out.cuda_stream))
 
     e2e_step()
     torch.cuda.synchronize()

@@ -228,8 +228,9 @@ int32_t th_pool_blocks(double* pool, double* compact, int64_t n_patches, int64_t
                        int32_t pack, void* stream);
 
 /* Copy n_boxes cell boxes (th_box records in DEVICE memory) from src to dst, both
- * device.  Boxes must not overlap one another's targets, nor a target overlap a
- * source of the same launch.  Bit-exact. */
+ * device.  Targets may overlap one another only where they write identical values
+ * (the multi-GPU unpack writes one fine patch's boxes for several orientations into
+ * one staging slot); no target may overlap a source of the same launch.  Bit-exact. */
 int32_t th_copy_boxes(const double* src, double* dst, const th_box* boxes, int64_t n_boxes, int32_t u,
                       void* stream);
 
