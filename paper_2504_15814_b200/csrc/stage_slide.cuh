@@ -326,7 +326,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
         const int zA = a2 - wA, zB = a2 - wB;
         const bool inA = zA >= 0 && zA < L, inB = zB >= 0 && zB < L;
         mbar_wait(&full[s], ph);
+#ifdef TH_AB_NOCOMPUTE  // diagnosis build: the producer's stream alone (consumers only hand slices back)
+        if (false) {
+#else
         if (active) {
+#endif
           const int* h = hdr + s * 4;
           const int XS = h[0], YS = h[1], BASE = h[2];
           const double* st = stages + size_t(s) * stage_d + BASE + cb + lane;

@@ -587,7 +587,9 @@ struct StageGeom {
   int nst = 0, stage_d = 0, ny_max = 0, tg = 0, tiles_per_face = 0, out_d = 0;
   size_t smem = 0;
 };
-constexpr int kRestrictNCW = 9, kRestrictNU = 2;  // restriction: one consumer warp per t1 group at u <= 64
+// restriction: one consumer warp per t1 group at u <= 64, two unknowns per lane (18 warps with one
+// unknown per lane measured 0.76 against 0.845 of the copy peak: profiles/r02_ab_restriction.txt)
+constexpr int kRestrictNCW = 9, kRestrictNU = 2;
 
 bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   const th::HostOperator& h = op->host;
