@@ -26,7 +26,7 @@ def env():
     return th, torch
 
 
-def _simulate(th, torch, world, straddle, faces_world=None):
+def _simulate(th, torch, world, straddle, faces_world=None, p=None, scheme="order3", scale=SCALE):
     """Sweep of config-5-shaped faces (generated for `faces_world` ranks) over `world`
     simulated ranks."""
     import dataclasses
@@ -34,11 +34,11 @@ def _simulate(th, torch, world, straddle, faces_world=None):
     import workloads as W
     from paper_2504_15814_b200.multigpu import LoopbackTransport, Partition, Support, make_rank_sweep, plan_sweep
 
-    wl0 = W.describe_multi(faces_world or world, scale=SCALE, straddle=straddle)
+    wl0 = W.describe_multi(faces_world or world, scale=scale, straddle=straddle, p=p)
     wl0 = dataclasses.replace(wl0, part=Partition(wl0.spec.n_patches, world))
     s = wl0.spec
     p, k, u = s.p, s.k, s.u
-    ops = {r: th.operators.DEFAULT_CACHE.device_operator(r, "order3", p, k) for r in ("interpolate", "restrict")}
+    ops = {r: th.operators.DEFAULT_CACHE.device_operator(r, scheme, p, k) for r in ("interpolate", "restrict")}
     support = Support.from_operators(ops["interpolate"], ops["restrict"], p, k)
     hub = LoopbackTransport(world)
     ranks = []
@@ -75,7 +75,7 @@ def _simulate(th, torch, world, straddle, faces_world=None):
     return wl0, results, kinds
 
 
-def _oracle_check(wl, results, kinds):
+def _oracle_check(wl, results, kinds, scheme="order3"):
     import workloads as W
     from oracle import exchange as OE
     from oracle import geometry as OG
@@ -87,7 +87,7 @@ def _oracle_check(wl, results, kinds):
     for (role, f), got in results.items():
         seg = int(wl.segment[f]) if role == "interpolate" else 0
         cfg = OG.FaceCfg("xyz"[int(wl.normal[f])], ("negative", "positive")[int(wl.side[f])], seg, s.p, s.k, s.u)
-        ex = OE.exchange_for(cfg, "order3", role)
+        ex = OE.exchange_for(cfg, scheme, role)
         jobs.append((ex, W.face_source(wl, f, role, patches), np.empty(ex.n_out), got.numpy(), kinds[(role, f)]))
     st = OE.run_many([j[0] for j in jobs], [j[1] for j in jobs], [j[2] for j in jobs], 8)
     assert (st == 0).all()
@@ -110,5 +110,21 @@ def test_simulated_ranks_match_oracle_and_single_rank(env, world, straddle):
     # where a face is computed does not change its arithmetic: bitwise equal to one rank
     _, res_1, kinds_1 = _simulate(th, torch, 1, straddle, faces_world=world)
     assert set(kinds_1.values()) == {"local"}
+    for key, v in res_n.items():
+        assert torch.equal(v, res_1[key]), key
+
+
+@pytest.mark.parametrize("p,scheme", [(17, "order3"), (17, "order2"), (9, "tensor_linear"), (9, "matrix_linear")])
+def test_simulated_ranks_other_schemes(env, p, scheme):
+    """The same cross-GPU path for the other schemes and for p = 17 (segments that cut coarse
+    blocks; source boxes of up to 11 x 11 cells): 3 simulated ranks with straddling faces."""
+    th, torch = env
+    scale = 0.0015 if p == 17 else SCALE
+    wl, res_n, kinds = _simulate(th, torch, 3, 0.15, p=p, scheme=scheme, scale=scale)
+    counts = {k: sum(1 for v in kinds.values() if v == k) for k in ("local", "staged", "received")}
+    assert counts["staged"] > 0 and counts["received"] > 0, counts
+    worst = _oracle_check(wl, res_n, kinds, scheme)
+    assert max(worst.values()) <= 1e-12, worst
+    _, res_1, _ = _simulate(th, torch, 1, 0.15, faces_world=3, p=p, scheme=scheme, scale=scale)
     for key, v in res_n.items():
         assert torch.equal(v, res_1[key]), key

@@ -347,7 +347,7 @@ class MultiWorkload:
 
 
 def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10, straddle: float = 0.0,
-                   fine_layout: str = "random") -> MultiWorkload:
+                   fine_layout: str = "random", p: int | None = None) -> MultiWorkload:
     """Global face list of config 5 (identical on every rank).
 
     BASELINE: 10% of faces have coarse and fine patches on different GPUs, the partner GPU
@@ -360,6 +360,8 @@ def describe_multi(world: int, scale: float = 1.0, cross: float = 0.10, straddle
     if scale != 1.0:
         spec = Spec(**{**spec.__dict__, "n_patches": max(8 * world, int(spec.n_patches * scale)),
                        "n_faces": max(12, int(spec.n_faces * scale))})
+    if p is not None and p != spec.p:  # tests: config-5-shaped faces at another patch size
+        spec = Spec(**{**spec.__dict__, "p": int(p)})
     rng = np.random.default_rng(spec.seed)
     fld = Field.make(spec.field, spec.u, rng)
     n, nf = spec.n_patches, spec.n_faces
