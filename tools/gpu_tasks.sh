@@ -24,7 +24,7 @@ for task in "$@"; do
                 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"tile3|stage_slide|strided_box|finite" -c 40 --csv --log-file gpurun_out/launches_c5.csv $cmd > gpurun_out/ncu_list.log 2>&1
                 cmd8="python bench.py --scale 0.125 --steps 1 --warmup 1 --no-e2e --no-cpu"
                 timeout 600 $cmd8 > gpurun_out/ncu_plain8.json 2>&1 &&
-                timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"tile3_interp|stage_slide" -s 2 -c 2 -o gpurun_out/prof_c5 -f $cmd8 > gpurun_out/ncu_full.log 2>&1
+                timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"tile3p|stage_slide" -s 2 -c 2 -o gpurun_out/prof_c5 -f $cmd8 > gpurun_out/ncu_full.log 2>&1
                 tail -2 gpurun_out/ncu_full.log ;;
     reftests)   # the reference's own tests against the drop-in (needs baseline/_ref/tests_ref, git-ignored)
                 timeout 1200 python tools/run_reference_tests.py baseline/_ref/tests_ref test_schemes.py -q > gpurun_out/reftests_schemes.log 2>&1; tail -3 gpurun_out/reftests_schemes.log
