@@ -1,0 +1,587 @@
+// Slice-ring interpolation for the Gram least-squares schemes (order2: 3-cell windows,
+// order3: 5-cell windows), included by trihalo.cu after tile_interp3.cuh.
+//
+// Same arithmetic as gram_slide_kernel<ORDER, 0> and the tiles of tile_interp3.cuh (the
+// reference's least-squares rows, taylor.py:171-219, as the projection onto total degree
+// <= ORDER with the window's discrete Gram polynomials, evaluated separably at the children),
+// organised as a stream of t2 slices instead of whole-face tiles, so that it also fits the
+// faces of large patches (p = 17: 6-7 blocks and 11 source cells per axis):
+//
+//  * a tile = (face, t1 part of <= 4 blocks, chunk of <= 32 unknowns); lanes run over the
+//    chunk's unknowns, so every table value is warp-uniform and every lane's data chain
+//    (source -> T -> children) is private to it;
+//  * "A" warps each own every NA-th t2 slice of the CTA's tile sequence: cp.async the slice
+//    (L x <= L + 3 cells) into a private staging slot one own-slice ahead, take the normal
+//    Gram moments of its lines and the t1 moments of every window start of the part, and
+//    write T[start][pair] into a slot of a ring of R slices;
+//  * "B" warps take the blocks (row r of the face, block b1 of the part) round-robin: wait for
+//    the L slices of the row's t2 window, take the block's t2 moments from the ring, release
+//    the row, synthesise the <= 27 children and store them;
+//  * hand-offs are mbarriers with one arrival per warp: full[slot] (the producing A warp),
+//    row[r mod 32] (every B warp, whether or not it had a block in the row: rows complete in
+//    order), hdr[tile mod 32] (tile headers decoded 8 tiles ahead by one A thread).  No warp
+//    ever waits for a warp of its own group, and an A warp only waits for the rows that read
+//    the slice it is about to overwrite.
+#pragma once
+
+constexpr int RG_NW = 16;                 // warps per CTA (one CTA per SM)
+constexpr int RG_NTH = RG_NW * 32;
+constexpr int RG_NS = 4;                  // blocks per row of a tile (t1 part)
+constexpr int RG_NH = 32;                 // header ring
+constexpr int RG_HAHEAD = 8;              // headers decoded ahead of the leading A iterator
+constexpr int RG_RR = 32;                 // row barriers
+constexpr int RG_RMAX = 32;               // T ring slots (upper bound)
+
+#ifndef RG_DIRECT
+#define RG_DIRECT 0                       // A warps load their slices straight into registers (0: cp.async staging)
+#endif
+#ifndef RG_PARTEST
+#define RG_PARTEST 0                      // B warps test a row's new slices together before falling back to waits
+#endif
+#ifndef RG_PFD
+#define RG_PFD 2                          // own slices between an A warp's projection and its L2 prefetch
+#endif
+#ifndef RG_WAIT_HINT
+#define RG_WAIT_HINT 0                    // suspend-time hint (ns) of the hand-off waits; 0: none
+#endif
+
+__device__ __forceinline__ void rg_wait(uint64_t* b, unsigned parity) {
+#if RG_WAIT_HINT > 0
+  asm volatile(
+      "{ .reg .pred P; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2; @!P bra WAIT_%=; }" ::"r"(
+          smem_u32(b)),
+      "r"(parity), "n"(RG_WAIT_HINT)
+      : "memory");
+#else
+  mbar_wait(b, parity);
+#endif
+}
+
+// wait of a warp that is ahead of its consumers (an A warp whose ring slot is still being
+// read): back off between tries, so that the spinning does not take shared-memory issue slots
+// from the warps it is waiting for
+#ifndef RG_SLEEP
+#define RG_SLEEP 200                      // ns between tries of an A warp's slot wait (0: plain try_wait loop)
+#endif
+__device__ __forceinline__ void rg_wait_relaxed(uint64_t* b, unsigned parity) {
+#if RG_SLEEP > 0
+  unsigned ok;
+  const unsigned a = smem_u32(b);
+  for (;;) {
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(RG_SLEEP);
+  }
+#else
+  rg_wait(b, parity);
+#endif
+}
+
+// non-blocking phase test
+__device__ __forceinline__ bool rg_test(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred P; mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+struct RingHdr {
+  int64_t src_off;     // source cell (normal window start, first t1 line / t2 slice of the part)
+  int64_t dst_off;     // target origin of the face
+  int64_t sn, s1, s2;  // signed source strides (reference frame)
+  int64_t dn, d1, d2;  // target strides
+  int lo1, lo2;        // target index origin of the segment along t1 / t2
+  int g1, n1, g2, n2;  // the part's blocks along t1, the face's rows along t2
+  int y0, ny, z0, nz;  // source lines / slices of the tile
+  int cb, cn;          // the tile's unknowns [cb, cb + cn)
+  int narrow;          // every target offset inside the face fits 32 bits
+  int snarrow;         // every source offset inside a slice fits 32 bits
+  int4 G0;             // the normal group
+};
+
+// tile = ((face, t1 part), chunk)
+template <int L>
+__device__ __forceinline__ void ring_decode(const DevOp& op, const th_face* __restrict__ faces, int64_t tile,
+                                            int ntp, int nch, int u, RingHdr& H) {
+  const int64_t st = tile / nch;
+  const int c = int(tile - st * nch);
+  const int64_t f = st / ntp;
+  const int tp = int(st - f * ntp);
+  FaceRef fr;
+  decode_face(faces + f, op, fr);
+  const int a1 = tp * fr.n1 / ntp, b1 = (tp + 1) * fr.n1 / ntp;
+  H.g1 = fr.g1 + a1;
+  H.n1 = b1 - a1;
+  H.g2 = fr.g2;
+  H.n2 = fr.n2;
+  H.dst_off = fr.dst;
+  H.sn = fr.sn;
+  H.s1 = fr.s1;
+  H.s2 = fr.s2;
+  H.dn = fr.dn;
+  H.d1 = fr.d1;
+  H.d2 = fr.d2;
+  H.lo1 = fr.lo1;
+  H.lo2 = fr.lo2;
+  H.cb = int(int64_t(c) * u / nch);
+  H.cn = int(int64_t(c + 1) * u / nch) - H.cb;
+  if (H.n1 <= 0 || H.n2 <= 0 || H.cn <= 0) {  // empty tile: no slices, no rows
+    H.n1 = H.n2 = 0;
+    H.y0 = H.z0 = H.ny = H.nz = 0;
+    H.cn = 0;
+  } else {
+    H.y0 = __ldg(&op.grp1[H.g1]).x;
+    H.ny = __ldg(&op.grp1[H.g1 + H.n1 - 1]).x + L - H.y0;
+    H.z0 = __ldg(&op.grp1[H.g2]).x;
+    H.nz = __ldg(&op.grp1[H.g2 + H.n2 - 1]).x + L - H.z0;
+  }
+  const int4 G0 = __ldg(&op.grp0[fr.g0]);
+  H.G0 = G0;
+  H.src_off = fr.src0 + int64_t(G0.x) * fr.sn + int64_t(H.y0) * fr.s1 + int64_t(H.z0) * fr.s2 + H.cb;
+  const int64_t lim = int64_t(1) << 21;
+  auto small = [lim](int64_t s) { return s > -lim && s < lim; };
+  H.narrow = small(fr.dn) && small(fr.d1) && small(fr.d2) && op.p <= 64 && u <= (1 << 20);
+  H.snarrow = small(fr.sn) && small(fr.s1) && op.p <= 64;
+}
+
+// position of an A warp in the CTA's slice stream: slice z of the it-th tile of the CTA
+struct RingIt {
+  int64_t tile;
+  int it;     // tiles of this CTA before `tile`
+  int z;      // slice of the tile
+  int gz;     // slices of this CTA before the tile
+  int slotb;  // ring slot of the tile's slice 0 and the parity of its use of that slot
+  int parb;
+  int rsb;    // rows of this CTA before the tile
+};
+
+// cp.async copies of slice z of a tile (all its t1 lines) into a staging slot, lanes over unknowns
+template <int L>
+__device__ __forceinline__ void ring_fetch(const RingHdr& H, const double* __restrict__ src, double* bslot, int bpitch,
+                                           int z) {
+  const int lane = threadIdx.x & 31;
+  if (lane >= H.cn) return;
+  const int64_t sn = H.sn, s1 = H.s1;
+  const double* const base = src + (H.src_off + lane + int64_t(z) * H.s2);
+  double* const bq = bslot + lane * bpitch;
+#pragma unroll 1
+  for (int y = 0; y < H.ny; ++y) {
+    const double* cell = base + int64_t(y) * s1;
+#pragma unroll
+    for (int x = 0; x < L; ++x, cell += sn) cp_async8(bq + L * y + x, cell);
+  }
+}
+
+// L2 prefetch of slice z of a tile: a cell per lane and iteration, the <= 3 lines of its chunk
+template <int L>
+__device__ __forceinline__ void ring_prefetch(const RingHdr& H, const double* __restrict__ src, int z) {
+  const int lane = threadIdx.x & 31;
+  const int n = L * H.ny, last = H.cn * 8 - 1;
+  const char* const base = reinterpret_cast<const char*>(src + (H.src_off + int64_t(z) * H.s2));
+#pragma unroll 1
+  for (int c = lane; c < n; c += 32) {
+    const int y = c / L, x = c - L * y;
+    const char* const pc = base + 8 * (int64_t(x) * H.sn + int64_t(y) * H.s1);
+    l2_prefetch_line(pc);
+    l2_prefetch_line(pc + 128);
+    l2_prefetch_line(pc + last);
+  }
+}
+
+// phase A of one slice: normal moments of its NY lines, t1 moments of every window start
+template <int L, int D, int NY>
+__device__ __forceinline__ void ring_phase_a(const double* bq, double* tq, double& chk) {
+  constexpr int NP = D * (D + 1) / 2;
+  double mm[NY][D];
+#pragma unroll
+  for (int y = 0; y < NY; ++y) {
+    double v[L];
+#pragma unroll
+    for (int x = 0; x < L; ++x) v[x] = bq[L * y + x];
+    gram_moments<L, D>(v, mm[y]);
+    asm volatile("" ::: "memory");  // one line of loads live at a time (register budget)
+  }
+#pragma unroll
+  for (int s = 0; s + L <= NY; ++s) {
+    double w[L][D];
+#pragma unroll
+    for (int y = 0; y < L; ++y)
+#pragma unroll
+      for (int a = 0; a < D; ++a) w[y][a] = mm[s + y][a];
+    double T[NP];
+    gram_y<L, D>(w, T);
+    // every value of the slice enters some window's T_00 (the windows cover the t1 extent)
+    chk = fma(T[0], 0.0, chk);
+#pragma unroll
+    for (int t = 0; t < NP; t += 2) *reinterpret_cast<double2*>(tq + s * NP + t) = make_double2(T[t], T[t + 1]);
+  }
+}
+
+// phase A with the slice's lines loaded straight from global memory (no staging slot): all
+// loads of the slice are independent, so the compiler issues them ahead of the moments
+template <int L, int D, int NY, typename SOFF>
+__device__ __forceinline__ void ring_phase_a_direct(const double* __restrict__ base, SOFF sn, SOFF s1, double* tq,
+                                                    double& chk) {
+  constexpr int NP = D * (D + 1) / 2;
+  double mm[NY][D];
+  {
+    double v[NY][L];
+#pragma unroll
+    for (int y = 0; y < NY; ++y)
+#pragma unroll
+      for (int x = 0; x < L; ++x) v[y][x] = __ldg(base + (SOFF(y) * s1 + SOFF(x) * sn));
+#pragma unroll
+    for (int y = 0; y < NY; ++y) gram_moments<L, D>(v[y], mm[y]);
+  }
+#pragma unroll
+  for (int s = 0; s + L <= NY; ++s) {
+    double w[L][D];
+#pragma unroll
+    for (int y = 0; y < L; ++y)
+#pragma unroll
+      for (int a = 0; a < D; ++a) w[y][a] = mm[s + y][a];
+    double T[NP];
+    gram_y<L, D>(w, T);
+    chk = fma(T[0], 0.0, chk);
+#pragma unroll
+    for (int t = 0; t < NP; t += 2) *reinterpret_cast<double2*>(tq + s * NP + t) = make_double2(T[t], T[t + 1]);
+  }
+}
+
+template <int L, int D, typename SOFF>
+__device__ __forceinline__ void ring_phase_a_direct_any(int ny, const double* __restrict__ base, SOFF sn, SOFF s1,
+                                                        double* tq, double& chk) {
+  if (ny == L) ring_phase_a_direct<L, D, L, SOFF>(base, sn, s1, tq, chk);
+  else if (ny == L + 1) ring_phase_a_direct<L, D, L + 1, SOFF>(base, sn, s1, tq, chk);
+  else if (ny == L + 2) ring_phase_a_direct<L, D, L + 2, SOFF>(base, sn, s1, tq, chk);
+  else if (ny == L + 3) ring_phase_a_direct<L, D, L + 3, SOFF>(base, sn, s1, tq, chk);
+}
+
+template <int L, int D>
+__device__ __forceinline__ void ring_phase_a_any(int ny, const double* bq, double* tq, double& chk) {
+  if (ny == L) ring_phase_a<L, D, L>(bq, tq, chk);
+  else if (ny == L + 1) ring_phase_a<L, D, L + 1>(bq, tq, chk);
+  else if (ny == L + 2) ring_phase_a<L, D, L + 2>(bq, tq, chk);
+  else if (ny == L + 3) ring_phase_a<L, D, L + 3>(bq, tq, chk);
+}
+
+// t2 moments of a block: the pairs (a, b) of its window start, L ring slices at zo[]
+// (moment index: a-major, then b, then c; D - a - b moments per pair)
+template <int L, int D>
+__device__ __forceinline__ void ring_moments(const double* tq, const int (&zo)[L], double* M) {
+  constexpr int NP = D * (D + 1) / 2;
+  static_assert(D == 3 || D == 4, "order2 / order3");
+  // pair t = (a, b), a-major: offset of its moments in M and their count D - a - b
+  constexpr int MO4[10] = {0, 4, 7, 9, 10, 13, 15, 16, 18, 19}, MN4[10] = {4, 3, 2, 1, 3, 2, 1, 2, 1, 1};
+  constexpr int MO3[6] = {0, 3, 5, 6, 8, 9}, MN3[6] = {3, 2, 1, 2, 1, 1};
+#pragma unroll
+  for (int t = 0; t < NP; t += 2) {
+    int mo0, mn0, mo1, mn1;
+    if constexpr (D == 4) mo0 = MO4[t], mn0 = MN4[t], mo1 = MO4[t + 1], mn1 = MN4[t + 1];
+    else mo0 = MO3[t], mn0 = MN3[t], mo1 = MO3[t + 1], mn1 = MN3[t + 1];
+    double ca[L], cb[L];
+#pragma unroll
+    for (int z = 0; z < L; ++z) {
+      const double2 v = *reinterpret_cast<const double2*>(tq + zo[z] + t);
+      ca[z] = v.x;
+      cb[z] = v.y;
+    }
+    gram_moments_n<L>(ca, M + mo0, mn0);
+    gram_moments_n<L>(cb, M + mo1, mn1);
+    asm volatile("" ::: "memory");  // one column pair of loads live at a time
+  }
+}
+
+// synthesis at the block's children and stores
+template <int D, bool ALL, typename OFF>
+__device__ __forceinline__ void ring_synth(const double* M, const T3Syn0& s0, const double* r1, const double* r2,
+                                           double* __restrict__ hdst, OFF qo, OFF d1, OFF d2, const OFF (&do0)[3],
+                                           const bool (&ok0)[3], const bool (&ok1)[3], const bool (&ok2)[3]) {
+  constexpr int NP = D * (D + 1) / 2;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    if (!ALL && !ok2[l]) continue;
+    asm volatile("" ::: "memory");  // table values re-read per child (not hoisted into registers)
+    double S2[4];
+    ld4(r2 + l * 4, S2);
+    double Q[NP];
+    int t = 0, mi = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b + a < D; ++b, ++t) {
+        Q[t] = 0.0;
+#pragma unroll
+        for (int c = 0; c + b + a < D; ++c, ++mi) Q[t] = fma(S2[c], M[mi], Q[t]);
+      }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (!ALL && !ok1[j]) continue;
+      asm volatile("" ::: "memory");  // S1 re-read per child
+      double S1[4];
+      ld4(r1 + j * 4, S1);
+      double R[D];
+      int tt = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        R[a] = 0.0;
+#pragma unroll
+        for (int b = 0; b + a < D; ++b, ++tt) R[a] = fma(S1[b], Q[tt], R[a]);
+      }
+      const OFF oj = qo + OFF(l) * d2 + OFF(j) * d1;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double oi = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) oi = fma(s0.v[i * 4 + a], R[a], oi);  // constant-bank operands
+        if (ALL || ok0[i]) *elem(hdst, oj + do0[i]) = oi;
+      }
+    }
+  }
+}
+
+// one block of a B warp (lane = unknown): the block's children from its moments M
+template <int D, typename OFF>
+__device__ __forceinline__ void ring_block(const RingHdr& H, const DevOp& op, double* __restrict__ dst, const double* M,
+                                           const double* stab, const T3Syn0& s0, int4 G1, int4 G2, int g1, int g2) {
+  const int4 G0 = H.G0;
+  bool ok0[3], ok1[3], ok2[3];
+  OFF do0[3];
+  bool all = true;
+  const int p = op.p;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int t = G0.z + i;
+    ok0[i] = i < G0.w && t >= 0 && t < op.k;
+    do0[i] = OFF(t) * OFF(H.dn);
+    ok1[i] = i < G1.w && unsigned(G1.z + i - H.lo1) < unsigned(p);
+    ok2[i] = i < G2.w && unsigned(G2.z + i - H.lo2) < unsigned(p);
+    all &= ok0[i] & ok1[i] & ok2[i];
+  }
+  const OFF d1 = OFF(H.d1), d2 = OFF(H.d2);
+  const int q = threadIdx.x & 31;
+  const OFF qo = OFF(G1.z - H.lo1) * d1 + OFF(G2.z - H.lo2) * d2 + OFF(H.cb + q);
+  double* const hdst = dst + H.dst_off;
+  const double* r1 = stab + g1 * 12;
+  const double* r2 = stab + g2 * 12;
+  if (all) ring_synth<D, true, OFF>(M, s0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+  else ring_synth<D, false, OFF>(M, s0, r1, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+}
+
+// dynamic shared memory: sgrp int4[G1] | stab [G1][12] | staging [NA][2][cmax][bpitch] | T ring [R][cmax][tpitch]
+__host__ __device__ inline int ring_fixed_doubles(int G1) { return 2 * G1 + ((G1 * 12 + 1) & ~1); }
+
+template <int ORDER>
+__global__ void __launch_bounds__(RG_NTH, 1)
+    ring_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
+                       const th_face* __restrict__ faces, int64_t n_tiles, int ntp, int nch, int cmax, int u, int NA,
+                       int R, int bpitch, int tpitch, int32_t* flag) {
+  constexpr int L = ORDER == 2 ? 3 : 5, D = ORDER + 1, NP = D * (D + 1) / 2, NM = ORDER == 2 ? 10 : 20;
+  extern __shared__ __align__(16) double smem_rg[];
+  __shared__ RingHdr Hs[RG_NH];
+  __shared__ __align__(8) uint64_t bar_full[RG_RMAX], bar_row[RG_RR], bar_hdr[RG_NH];
+  __shared__ int lastrow[RG_RMAX];
+
+  const int G1n = op.G1;
+  int4* const sgrp = reinterpret_cast<int4*>(smem_rg);
+  double* const stab = smem_rg + 2 * G1n;
+  const int boxd = (cmax * bpitch + 1) & ~1, trd = cmax * tpitch;
+  double* const box0 = smem_rg + ring_fixed_doubles(G1n);
+  double* const tr0 = box0 + (RG_DIRECT ? 0 : NA * 2 * boxd);
+  const int NB = RG_NW - NA;
+  for (int i = threadIdx.x; i < G1n; i += RG_NTH) sgrp[i] = __ldg(&op.grp1[i]);
+  for (int i = threadIdx.x; i < G1n * 12; i += RG_NTH) stab[i] = __ldg(op.synth1 + i);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RG_RMAX; ++i) mbar_init(&bar_full[i], 1);
+    for (int i = 0; i < RG_RR; ++i) mbar_init(&bar_row[i], NB);
+    for (int i = 0; i < RG_NH; ++i) mbar_init(&bar_hdr[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t0 = blockIdx.x, step = gridDim.x;
+
+  if (warp < NA) {
+    // ============ A warps: fetch, phase A of every NA-th slice ============
+    const bool scout = warp == 0 && lane == 0;  // decodes the tile headers
+    if (scout)
+      for (int i = 0; i < RG_HAHEAD; ++i)
+        if (t0 + i * step < n_tiles) {
+          ring_decode<L>(op, faces, t0 + i * step, ntp, nch, u, Hs[i]);
+          mbar_arrive(&bar_hdr[i]);
+        }
+    // move an iterator whose z ran past its tile to the tile holding that slice; the leading
+    // iterator waits for (and the scout decodes) headers, the others follow it
+    auto settle = [&](RingIt& I, bool lead) {
+      while (I.tile < n_tiles) {
+        const RingHdr& H = Hs[I.it & (RG_NH - 1)];
+        if (I.z < H.nz) break;
+        I.z -= H.nz;
+        I.gz += H.nz;
+        I.slotb += H.nz;
+        if (I.slotb >= R) I.slotb -= R, I.parb ^= 1;
+        I.rsb += H.n2;
+        I.tile += step;
+        ++I.it;
+        if (lead && I.tile < n_tiles) {
+          const int64_t nt = I.tile + int64_t(RG_HAHEAD - 1) * step;
+          const int ni = I.it + RG_HAHEAD - 1;
+          if (scout && nt < n_tiles) {
+            ring_decode<L>(op, faces, nt, ntp, nch, u, Hs[ni & (RG_NH - 1)]);
+            mbar_arrive(&bar_hdr[ni & (RG_NH - 1)]);
+          }
+          __syncwarp();
+          rg_wait(&bar_hdr[I.it & (RG_NH - 1)], (I.it / RG_NH) & 1);
+        }
+      }
+    };
+    // P: the slice being projected, F: the next own slice (its copies are in flight), G: the own
+    // slice RG_PFD ahead of P, whose lines are being pulled into L2
+    RingIt G{t0, 0, warp, 0, 0, 0, 0};
+    if (t0 < n_tiles) rg_wait(&bar_hdr[0], 0);
+    settle(G, true);
+    RingIt P = G;
+    const bool pf = (op.prefetch & 16) != 0;
+    for (int i = 0; i < RG_PFD; ++i) {
+      if (pf && i >= (RG_DIRECT ? 1 : 2) && G.tile < n_tiles) ring_prefetch<L>(Hs[G.it & (RG_NH - 1)], src, G.z);
+      G.z += NA;
+      settle(G, true);
+    }
+#if !RG_DIRECT
+    RingIt F = P;
+    F.z += NA;
+    settle(F, false);
+    double* const mybox = box0 + warp * 2 * boxd;
+    if (P.tile < n_tiles) ring_fetch<L>(Hs[P.it & (RG_NH - 1)], src, mybox, bpitch, P.z);
+    cp_async_commit();
+    if (F.tile < n_tiles) ring_fetch<L>(Hs[F.it & (RG_NH - 1)], src, mybox + boxd, bpitch, F.z);
+    cp_async_commit();
+#endif
+    if (pf && G.tile < n_tiles) ring_prefetch<L>(Hs[G.it & (RG_NH - 1)], src, G.z);
+    double chk = 0.0;
+    int k = 0;
+    while (P.tile < n_tiles) {
+#if !RG_DIRECT
+      cp_async_wait_one();  // this thread's copies of slice P landed
+#endif
+      const RingHdr& H = Hs[P.it & (RG_NH - 1)];
+      int s = P.slotb + P.z, par = P.parb;
+      if (s >= R) s -= R, par ^= 1;
+      if (P.gz + P.z >= R) {
+        // the slot's previous slice: produced (its lastrow entry is visible) and read by every
+        // row that uses it
+        rg_wait(&bar_full[s], par ^ 1);
+        const int need = lastrow[s];
+        rg_wait_relaxed(&bar_row[need & (RG_RR - 1)], (need / RG_RR) & 1);
+      }
+#if RG_DIRECT
+      if (lane < H.cn) {
+        const double* const base = src + (H.src_off + lane + int64_t(P.z) * H.s2);
+        double* const tq = tr0 + s * trd + lane * tpitch;
+        if (H.snarrow) ring_phase_a_direct_any<L, D, int>(H.ny, base, int(H.sn), int(H.s1), tq, chk);
+        else ring_phase_a_direct_any<L, D, int64_t>(H.ny, base, H.sn, H.s1, tq, chk);
+      }
+#else
+      if (lane < H.cn)
+        ring_phase_a_any<L, D>(H.ny, mybox + (k & 1) * boxd + lane * bpitch, tr0 + s * trd + lane * tpitch, chk);
+#endif
+      // last row of the tile whose t2 window holds this slice
+      int lr = 0;
+      for (int r = 1; r < H.n2; ++r)
+        if (sgrp[H.g2 + r].x - H.z0 <= P.z) lr = r;
+      __syncwarp();
+      if (lane == 0) {
+        lastrow[s] = P.rsb + lr;
+        mbar_arrive(&bar_full[s]);
+      }
+#if RG_DIRECT
+      P.z += NA;
+      settle(P, false);
+#else
+      P = F;
+      F.z += NA;
+      settle(F, false);
+      if (F.tile < n_tiles) ring_fetch<L>(Hs[F.it & (RG_NH - 1)], src, mybox + (k & 1) * boxd, bpitch, F.z);
+      cp_async_commit();
+#endif
+      G.z += NA;
+      settle(G, true);
+      if (pf && G.tile < n_tiles) ring_prefetch<L>(Hs[G.it & (RG_NH - 1)], src, G.z);
+      ++k;
+    }
+#if !RG_DIRECT
+    cp_async_wait_all();
+#endif
+    raise_flag(flag, !isfinite(chk));
+  } else {
+    // ============ B warps: blocks round-robin, rows in order ============
+    const int bw = warp - NA;
+    int rs = 0, seq = 0, slotb = 0, parb = 0, it = 0;
+    for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
+      rg_wait(&bar_hdr[it & (RG_NH - 1)], (it / RG_NH) & 1);
+      const RingHdr& H = Hs[it & (RG_NH - 1)];
+      const int n1 = H.n1, n2 = H.n2;
+      int hi = -1;  // highest slice of the tile this warp has waited for
+#pragma unroll 1
+      for (int r = 0; r < n2; ++r, ++rs) {
+        int b1 = bw - seq;
+        if (b1 < 0) b1 += NB;
+        seq += n1;
+        if (seq >= NB) seq -= NB;
+        // every B warp observes every slice once, in order (a warp that ran a whole ring ahead
+        // of the producers would mistake a slot's previous use for the one it waits for)
+        const int4 G2 = sgrp[H.g2 + r];
+        const int dz = G2.x - H.z0;
+        // (all tests issued together first: a satisfied try_wait still costs a shared-memory
+        //  round trip, and the producers are usually ahead)
+        bool ready = RG_PARTEST != 0;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          int s = slotb + dz + j, par = parb;
+          if (s >= R) s -= R, par ^= 1;
+          if (RG_PARTEST && dz + j > hi) ready &= rg_test(&bar_full[s], par);
+        }
+        if (!ready) {
+#pragma unroll 1
+          for (int z = max(hi + 1, dz); z < dz + L; ++z) {
+            int s = slotb + z, par = parb;
+            if (s >= R) s -= R, par ^= 1;
+            rg_wait(&bar_full[s], par);
+          }
+        }
+        hi = dz + L - 1;
+        if (b1 >= n1) {
+          if (lane == 0) mbar_arrive(&bar_row[rs & (RG_RR - 1)]);
+          continue;
+        }
+        const int g1 = H.g1 + b1, g2 = H.g2 + r;
+        const int4 G1 = sgrp[g1];
+        int zo[L];
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          int s = slotb + dz + j;
+          if (s >= R) s -= R;
+          zo[j] = s * trd;
+        }
+        const bool active = lane < H.cn;
+        double M[NM];
+        if (active) ring_moments<L, D>(tr0 + lane * tpitch + (G1.x - H.y0) * NP, zo, M);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_row[rs & (RG_RR - 1)]);  // the row's slices are read
+        if (active) {
+          if (H.narrow) ring_block<D, int>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
+          else ring_block<D, int64_t>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
+        }
+      }
+      slotb += H.nz;
+      if (slotb >= R) slotb -= R, parb ^= 1;
+    }
+  }
+}

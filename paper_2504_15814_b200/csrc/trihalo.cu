@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(128) tensor_apply_kernel(DevOp op, const doubl
 #include "stage_slide.cuh"
 #include "tile_interp.cuh"
 #include "tile_interp3.cuh"
+#include "ring_interp.cuh"
 
 __global__ void finite_kernel(const double* __restrict__ v, int64_t n, int32_t* flag) {
   bool bad = false;
@@ -394,6 +395,9 @@ struct th_operator {
   // staged order3 tile interpolation (tile_interp3.cuh) eligibility
   bool t3_ok = false;
   int t3_nt = 1;
+  // slice-ring interpolation (ring_interp.cuh): window length (0 = not eligible), t1 parts per
+  // face, and the largest line / window-start / slice counts of a tile
+  int rg_L = 0, rg_ntp = 1, rg_nymax = 0, rg_nsmax = 0, rg_nzmax = 0;
 };
 
 namespace {
@@ -581,6 +585,56 @@ void prepare_tile3(th_operator* op) {
   op->t3_ok = true;
 }
 
+// Slice-ring interpolation (ring_interp.cuh): Gram least squares with one normal group of
+// 3 children, full windows of L = 3 / 5 cells on every tangential group, window starts
+// non-decreasing in steps of <= 1 (so every source slice lies in some row's window).  A
+// segment's blocks along t1 split into rg_ntp balanced parts of <= RG_NS blocks whose lines
+// span <= L + 3 cells.
+void prepare_ring(th_operator* op) {
+  const th::HostOperator& h = op->host;
+  op->rg_L = 0;
+  if (h.role != 0 || (h.scheme != TH_SCHEME_ORDER2 && h.scheme != TH_SCHEME_ORDER3) || !h.gram_ok ||
+      h.fast_C0 != 3 || h.synth[0].size() < 12 || h.synth[1].empty() || h.groups[0].size() != 1 ||
+      h.groups[1].empty())
+    return;
+  const int L = h.scheme == TH_SCHEME_ORDER2 ? 3 : 5;
+  const th::Group& g0 = h.groups[0][0];
+  if (g0.winL != L || g0.tgtN < 1 || g0.tgtN > 3) return;
+  const auto& g1 = h.groups[1];
+  for (size_t j = 0; j < g1.size(); ++j) {
+    if (g1[j].winL != L || g1[j].tgtN < 1 || g1[j].tgtN > 3) return;
+    if (j > 0 && (g1[j].win0 < g1[j - 1].win0 || g1[j].win0 > g1[j - 1].win0 + 1)) return;
+  }
+  int nmax = 0;
+  for (int c = 0; c < 3; ++c) nmax = std::max(nmax, h.seg_g[c][1] - h.seg_g[c][0]);
+  if (nmax < 1) return;
+  for (int ntp = (nmax + RG_NS - 1) / RG_NS; ntp <= nmax; ++ntp) {
+    bool ok = true;
+    int nymax = 0, nsmax = 0, nzmax = 0;
+    for (int c = 0; c < 3 && ok; ++c) {
+      const int a0 = h.seg_g[c][0], n = h.seg_g[c][1] - a0;
+      if (n < 1) continue;
+      nzmax = std::max(nzmax, g1[a0 + n - 1].win0 + L - g1[a0].win0);
+      for (int t = 0; t < ntp && ok; ++t) {
+        const int a = a0 + t * n / ntp, b = a0 + (t + 1) * n / ntp;
+        if (b <= a) continue;
+        const int ny = g1[b - 1].win0 + L - g1[a].win0;
+        ok = b - a <= RG_NS && ny <= L + 3;
+        nymax = std::max(nymax, ny);
+        nsmax = std::max(nsmax, ny - L + 1);
+      }
+    }
+    if (ok) {
+      op->rg_L = L;
+      op->rg_ntp = ntp;
+      op->rg_nymax = nymax;
+      op->rg_nsmax = nsmax;
+      op->rg_nzmax = nzmax;
+      return;
+    }
+  }
+}
+
 // launch geometry of the slice-staged kernels (stage_slide.cuh) for u unknowns;
 // false = the operator / u does not fit them
 struct StageGeom {
@@ -730,6 +784,7 @@ static int32_t operator_create(int32_t role, int32_t scheme, int32_t p, int32_t 
   prepare_stage(op);
   prepare_tile(op);
   prepare_tile3(op);
+  prepare_ring(op);
   if (!upload_to_device) {
     *out = op;
     return TH_OK;
@@ -902,6 +957,47 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   const bool gram = h.gram_ok && h.fast_C0 == 3;
   const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
   static const int use_tile = [] { const char* e = std::getenv("TH_TILE"); return e ? std::atoi(e) : 1; }();
+  //   TH_RING bits (default 0)   1: order3 interpolation through the slice ring (ring_interp.cuh)
+  //                              2: order2 interpolation through the slice ring
+  //   TH_RING_NA                 A warps of the slice ring (default: by blocks per row)
+  static const int use_ring = [] { const char* e = std::getenv("TH_RING"); return e ? std::atoi(e) : 0; }();
+  static const int ring_na = [] { const char* e = std::getenv("TH_RING_NA"); return e ? std::atoi(e) : 0; }();
+  if (interp && op->rg_L && (use_ring & (op->rg_L == 5 ? 1 : 2))) {
+    const int L = op->rg_L, NP = L == 5 ? 10 : 6;
+    const int nch = (u + 31) / 32;
+    int cmax = 0;
+    for (int c = 0; c < nch; ++c) cmax = std::max(cmax, int(int64_t(c + 1) * u / nch - int64_t(c) * u / nch));
+    const int NA = std::min(std::max(ring_na > 0 ? ring_na : (op->rg_nsmax <= 3 ? 6 : 5), 1), RG_NW - RG_NS);
+    const int bpitch = (L * op->rg_nymax) | 1;
+    int tpitch = op->rg_nsmax * NP;
+    while (tpitch % 4 != 2) ++tpitch;  // 16-byte accesses of consecutive lanes conflict-free
+    const int64_t boxd = (int64_t(cmax) * bpitch + 1) & ~int64_t(1), trd = int64_t(cmax) * tpitch;
+    const void* kfn = L == 5 ? reinterpret_cast<const void*>(ring_interp_kernel<3>)
+                             : reinterpret_cast<const void*>(ring_interp_kernel<2>);
+    int per_sm = 0;
+    const size_t fixed = 8 * (size_t(ring_fixed_doubles(op->dev.G1)) + (RG_DIRECT ? 0 : size_t(NA) * 2 * boxd));
+    TH_CUDA(resident_ctas(kfn, RG_NTH, fixed + 8 * size_t(trd) * (L + 1), &per_sm));
+    cudaFuncAttributes fa;
+    TH_CUDA(cudaFuncGetAttributes(&fa, kfn));
+    const int64_t avail = int64_t(fa.maxDynamicSharedSizeBytes) - int64_t(fixed);
+    static const int ring_r = [] { const char* e = std::getenv("TH_RING_R"); return e ? std::atoi(e) : RG_RMAX; }();
+    const int R = int(std::min<int64_t>(std::min(ring_r, RG_RMAX), avail / (8 * trd)));
+    if (per_sm >= 1 && R >= std::max(op->rg_nzmax, L + 1) && R >= NA) {
+      const size_t smem = fixed + 8 * size_t(trd) * R;
+      const int64_t tiles = n_faces * int64_t(op->rg_ntp) * nch;
+      const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms())));
+      T3Syn0 syn0;
+      std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
+      if (L == 5)
+        ring_interp_kernel<3><<<tblocks, RG_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, op->rg_ntp, nch,
+                                                            cmax, u, NA, R, bpitch, tpitch, flag);
+      else
+        ring_interp_kernel<2><<<tblocks, RG_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, op->rg_ntp, nch,
+                                                            cmax, u, NA, R, bpitch, tpitch, flag);
+      TH_CUDA(cudaGetLastError());
+      return TH_OK;
+    }
+  }
   if (use_tile && interp && op->ti_mode) {
     const int nt = op->ti_nt;
     const int pitch = TBOX | 1;

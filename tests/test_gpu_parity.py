@@ -355,7 +355,8 @@ def test_pool_transposed_layout(th, scheme, p):
 
 
 @pytest.mark.parametrize("env", ({"TH_GRAM": "3"}, {"TH_TILE": "0"}, {"TH_TILE3": "0"},
-                                 {"TH_TILE": "0", "TH_GRAM": "0"}))
+                                 {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_RING": "3"},
+                                 {"TH_RING": "3", "TH_RING_NA": "3"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
     parity tests in a child process with the alternative paths (the per-warp order3
