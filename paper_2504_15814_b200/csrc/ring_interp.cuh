@@ -81,6 +81,20 @@ __device__ __forceinline__ void rg_wait_relaxed(uint64_t* b, unsigned parity) {
 #endif
 }
 
+// slot sequence numbers: ready[slot] = 1 + index (in the CTA's slice stream) of the slice the
+// slot holds.  Written by the producing A warp after its T values (fence + volatile store),
+// polled by the B warps with acquire loads (plain LDS in SASS; all L slots of a row in flight
+// together; a fence here would wait for the warp's outstanding stores): unlike a phase bit, a sequence number cannot be mistaken for the slot's
+// previous use, so a B warp only looks at the slices of the rows it has a block in.
+__device__ __forceinline__ int lds_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_volatile(int* p, int v) {
+  asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 // non-blocking phase test
 __device__ __forceinline__ bool rg_test(uint64_t* b, unsigned parity) {
   unsigned ok;
@@ -386,8 +400,8 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   constexpr int L = ORDER == 2 ? 3 : 5, D = ORDER + 1, NP = D * (D + 1) / 2, NM = ORDER == 2 ? 10 : 20;
   extern __shared__ __align__(16) double smem_rg[];
   __shared__ RingHdr Hs[RG_NH];
-  __shared__ __align__(8) uint64_t bar_full[RG_RMAX], bar_row[RG_RR], bar_hdr[RG_NH];
-  __shared__ int lastrow[RG_RMAX];
+  __shared__ __align__(8) uint64_t bar_row[RG_RR], bar_hdr[RG_NH];
+  __shared__ int ready[RG_RMAX], lastrow[RG_RMAX];
 
   const int G1n = op.G1;
   int4* const sgrp = reinterpret_cast<int4*>(smem_rg);
@@ -399,7 +413,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   for (int i = threadIdx.x; i < G1n; i += RG_NTH) sgrp[i] = __ldg(&op.grp1[i]);
   for (int i = threadIdx.x; i < G1n * 12; i += RG_NTH) stab[i] = __ldg(op.synth1 + i);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < RG_RMAX; ++i) mbar_init(&bar_full[i], 1);
+    for (int i = 0; i < RG_RMAX; ++i) ready[i] = 0;
     for (int i = 0; i < RG_RR; ++i) mbar_init(&bar_row[i], NB);
     for (int i = 0; i < RG_NH; ++i) mbar_init(&bar_hdr[i], 1);
     mbar_fence_init();
@@ -472,12 +486,14 @@ __global__ void __launch_bounds__(RG_NTH, 1)
       cp_async_wait_one();  // this thread's copies of slice P landed
 #endif
       const RingHdr& H = Hs[P.it & (RG_NH - 1)];
-      int s = P.slotb + P.z, par = P.parb;
-      if (s >= R) s -= R, par ^= 1;
-      if (P.gz + P.z >= R) {
-        // the slot's previous slice: produced (its lastrow entry is visible) and read by every
-        // row that uses it
-        rg_wait(&bar_full[s], par ^ 1);
+      int s = P.slotb + P.z;
+      if (s >= R) s -= R;
+      const int gz = P.gz + P.z;
+      if (gz >= R) {
+        // the slot's previous slice was produced long ago (its rows ran): the fence makes its
+        // lastrow entry visible, then wait until every row that uses it has been read
+        while (lds_acquire(&ready[s]) != gz - R + 1) {
+        }
         const int need = lastrow[s];
         rg_wait_relaxed(&bar_row[need & (RG_RR - 1)], (need / RG_RR) & 1);
       }
@@ -499,7 +515,8 @@ __global__ void __launch_bounds__(RG_NTH, 1)
       __syncwarp();
       if (lane == 0) {
         lastrow[s] = P.rsb + lr;
-        mbar_arrive(&bar_full[s]);
+        __threadfence_block();
+        sts_volatile(&ready[s], gz + 1);
       }
 #if RG_DIRECT
       P.z += NA;
@@ -523,52 +540,42 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   } else {
     // ============ B warps: blocks round-robin, rows in order ============
     const int bw = warp - NA;
-    int rs = 0, seq = 0, slotb = 0, parb = 0, it = 0;
+    int rs = 0, seq = 0, slotb = 0, gzb = 0, it = 0;
     for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
       rg_wait(&bar_hdr[it & (RG_NH - 1)], (it / RG_NH) & 1);
       const RingHdr& H = Hs[it & (RG_NH - 1)];
       const int n1 = H.n1, n2 = H.n2;
-      int hi = -1;  // highest slice of the tile this warp has waited for
 #pragma unroll 1
       for (int r = 0; r < n2; ++r, ++rs) {
         int b1 = bw - seq;
         if (b1 < 0) b1 += NB;
         seq += n1;
         if (seq >= NB) seq -= NB;
-        // every B warp observes every slice once, in order (a warp that ran a whole ring ahead
-        // of the producers would mistake a slot's previous use for the one it waits for)
-        const int4 G2 = sgrp[H.g2 + r];
-        const int dz = G2.x - H.z0;
-        // (all tests issued together first: a satisfied try_wait still costs a shared-memory
-        //  round trip, and the producers are usually ahead)
-        bool ready = RG_PARTEST != 0;
-#pragma unroll
-        for (int j = 0; j < L; ++j) {
-          int s = slotb + dz + j, par = parb;
-          if (s >= R) s -= R, par ^= 1;
-          if (RG_PARTEST && dz + j > hi) ready &= rg_test(&bar_full[s], par);
-        }
-        if (!ready) {
-#pragma unroll 1
-          for (int z = max(hi + 1, dz); z < dz + L; ++z) {
-            int s = slotb + z, par = parb;
-            if (s >= R) s -= R, par ^= 1;
-            rg_wait(&bar_full[s], par);
-          }
-        }
-        hi = dz + L - 1;
+        // a warp arrives at the rows in order and never more than 24 rows ahead of the slowest
+        // B warp (the row barriers are reused every RG_RR = 32 rows)
+        if ((rs & 7) == 0 && rs >= 16) rg_wait(&bar_row[(rs - 16) & (RG_RR - 1)], ((rs - 16) / RG_RR) & 1);
         if (b1 >= n1) {
           if (lane == 0) mbar_arrive(&bar_row[rs & (RG_RR - 1)]);
           continue;
         }
+        const int4 G2 = sgrp[H.g2 + r];
+        const int dz = G2.x - H.z0;
         const int g1 = H.g1 + b1, g2 = H.g2 + r;
         const int4 G1 = sgrp[g1];
-        int zo[L];
+        int zo[L], sl[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) {
           int s = slotb + dz + j;
           if (s >= R) s -= R;
+          sl[j] = s;
           zo[j] = s * trd;
+        }
+        // the row's L slices: all polls in flight together
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int j = 0; j < L; ++j) ok &= lds_acquire(&ready[sl[j]]) == gzb + dz + j + 1;
+          if (ok) break;
         }
         const bool active = lane < H.cn;
         double M[NM];
@@ -581,7 +588,8 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         }
       }
       slotb += H.nz;
-      if (slotb >= R) slotb -= R, parb ^= 1;
+      if (slotb >= R) slotb -= R;
+      gzb += H.nz;
     }
   }
 }

@@ -957,17 +957,20 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   const bool gram = h.gram_ok && h.fast_C0 == 3;
   const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
   static const int use_tile = [] { const char* e = std::getenv("TH_TILE"); return e ? std::atoi(e) : 1; }();
-  //   TH_RING bits (default 0)   1: order3 interpolation through the slice ring (ring_interp.cuh)
-  //                              2: order2 interpolation through the slice ring
-  //   TH_RING_NA                 A warps of the slice ring (default: by blocks per row)
-  static const int use_ring = [] { const char* e = std::getenv("TH_RING"); return e ? std::atoi(e) : 0; }();
+  //   TH_RING bits (default 3)   1: order3 interpolation through the slice ring (ring_interp.cuh)
+  //                                 where the order3 tiles do not fit (p = 17)
+  //                              2: order2 interpolation likewise, where the 3-cell tiles do not fit
+  //                              4: the slice ring instead of the tile kernels wherever it fits
+  //   TH_RING_NA, TH_RING_R      A warps / ring slots of the slice ring (defaults: 7 A warps for
+  //                              rows of <= 3 blocks, 5 otherwise; as many slots as fit)
+  static const int use_ring = [] { const char* e = std::getenv("TH_RING"); return e ? std::atoi(e) : 3; }();
   static const int ring_na = [] { const char* e = std::getenv("TH_RING_NA"); return e ? std::atoi(e) : 0; }();
-  if (interp && op->rg_L && (use_ring & (op->rg_L == 5 ? 1 : 2))) {
+  auto ring_launch = [&]() -> int32_t {
     const int L = op->rg_L, NP = L == 5 ? 10 : 6;
     const int nch = (u + 31) / 32;
     int cmax = 0;
     for (int c = 0; c < nch; ++c) cmax = std::max(cmax, int(int64_t(c + 1) * u / nch - int64_t(c) * u / nch));
-    const int NA = std::min(std::max(ring_na > 0 ? ring_na : (op->rg_nsmax <= 3 ? 6 : 5), 1), RG_NW - RG_NS);
+    const int NA = std::min(std::max(ring_na > 0 ? ring_na : (op->rg_nsmax <= 3 ? 7 : 5), 1), RG_NW - RG_NS);
     const int bpitch = (L * op->rg_nymax) | 1;
     int tpitch = op->rg_nsmax * NP;
     while (tpitch % 4 != 2) ++tpitch;  // 16-byte accesses of consecutive lanes conflict-free
@@ -997,6 +1000,12 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
+    return -1;  // does not fit: the caller falls through to the next kernel
+  };
+  const bool ring_ok = interp && op->rg_L && (use_ring & (op->rg_L == 5 ? 1 : 2));
+  if (ring_ok && (use_ring & 4)) {
+    const int32_t rc = ring_launch();
+    if (rc >= 0) return rc;
   }
   if (use_tile && interp && op->ti_mode) {
     const int nt = op->ti_nt;
@@ -1045,6 +1054,10 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       TH_CUDA(cudaGetLastError());
       return TH_OK;
     }
+  }
+  if (ring_ok) {
+    const int32_t rc = ring_launch();
+    if (rc >= 0) return rc;
   }
   StageGeom sg;
   if ((use_gram & 8) && interp && tensor_fast) {

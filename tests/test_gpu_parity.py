@@ -355,14 +355,16 @@ def test_pool_transposed_layout(th, scheme, p):
 
 
 @pytest.mark.parametrize("env", ({"TH_GRAM": "3"}, {"TH_TILE": "0"}, {"TH_TILE3": "0"},
-                                 {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_RING": "3"},
-                                 {"TH_RING": "3", "TH_RING_NA": "3"}))
+                                 {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_RING": "7"},
+                                 {"TH_RING": "7", "TH_RING_NA": "3", "TH_RING_R": "6"}, {"TH_RING": "0"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
     parity tests in a child process with the alternative paths (the per-warp order3
     restriction slide; the per-warp interpolation slide instead of the staged tile kernel;
     the per-warp slide for order3 interpolation instead of the two-phase order3 tiles; the
-    fixed-window kernels with neither tiles nor Gram slides)."""
+    fixed-window kernels with neither tiles nor Gram slides; the slice ring (ring_interp.cuh)
+    for every order2 / order3 interpolation, also with 3 A warps and the smallest ring; the
+    per-warp slide instead of the slice ring at p = 17)."""
     import os
     import subprocess
     import sys

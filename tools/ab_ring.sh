@@ -7,7 +7,7 @@ sel="exchange_all_faces_small or pool_interp_batch or pool_restrict_batch or tra
 if [ "$mode" = parity ]; then
   for na in "$@"; do
     echo "== parity TH_RING=3 NA=$na"
-    TH_RING=3 TH_RING_NA=$na timeout 600 python -m pytest -q -x -m gpu tests/test_gpu_parity.py -k "$sel" 2>&1 | tail -4
+    TH_RING=7 TH_RING_NA=$na timeout 600 python -m pytest -q -x -m gpu tests/test_gpu_parity.py -k "$sel" 2>&1 | tail -4
   done
 else
   for cfg in 3 4; do
@@ -16,7 +16,7 @@ else
     python tools/bench_brief.py gpurun_out/ring_c${cfg}_def.json | grep -E "interpolate|parity"
     for na in "$@"; do
       echo "== config $cfg TH_RING=3 NA=$na"
-      TH_RING=3 TH_RING_NA=$na timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu --no-same-level > gpurun_out/ring_c${cfg}_na$na.json 2> gpurun_out/ring_c${cfg}_na$na.err
+      TH_RING=7 TH_RING_NA=$na timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu --no-same-level > gpurun_out/ring_c${cfg}_na$na.json 2> gpurun_out/ring_c${cfg}_na$na.err
       tail -2 gpurun_out/ring_c${cfg}_na$na.err
       python tools/bench_brief.py gpurun_out/ring_c${cfg}_na$na.json | grep -E "interpolate|parity"
     done
