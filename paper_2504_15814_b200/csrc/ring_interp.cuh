@@ -16,12 +16,12 @@
 //    write T[start][pair] into a slot of a ring of R slices;
 //  * "B" warps take the blocks (row r of the face, block b1 of the part) round-robin: wait for
 //    the L slices of the row's t2 window, take the block's t2 moments from the ring, release
-//    the row, synthesise the <= 27 children and store them;
-//  * hand-offs are mbarriers with one arrival per warp: full[slot] (the producing A warp),
-//    row[r mod 32] (every B warp, whether or not it had a block in the row: rows complete in
-//    order), hdr[tile mod 32] (tile headers decoded 8 tiles ahead by one A thread).  No warp
-//    ever waits for a warp of its own group, and an A warp only waits for the rows that read
-//    the slice it is about to overwrite.
+//    the slices, synthesise the <= 27 children and store them;
+//  * hand-offs: ready[slot] sequence numbers (written by the producing A warp, polled by the
+//    blocks that read the slice), free[slot] mbarriers counting the slice's readers down
+//    (transaction count), hdr[tile mod 32] (tile headers decoded 8 tiles ahead by one A
+//    thread).  No warp ever waits for a warp of its own group, and an A warp only waits for
+//    the blocks that read the slice it is about to overwrite.
 #pragma once
 
 constexpr int RG_NW = 16;                 // warps per CTA (one CTA per SM)
@@ -29,7 +29,6 @@ constexpr int RG_NTH = RG_NW * 32;
 constexpr int RG_NS = 4;                  // blocks per row of a tile (t1 part)
 constexpr int RG_NH = 32;                 // header ring
 constexpr int RG_HAHEAD = 8;              // headers decoded ahead of the leading A iterator
-constexpr int RG_RR = 32;                 // row barriers
 constexpr int RG_RMAX = 32;               // T ring slots (upper bound)
 
 #ifndef RG_DIRECT
@@ -93,6 +92,17 @@ __device__ __forceinline__ int lds_acquire(const int* p) {
 }
 __device__ __forceinline__ void sts_volatile(int* p, int v) {
   asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+// slot release: the producing A warp arrives on free[slot] with a pending transaction count =
+// the number of blocks that will read the slice; every reader takes one off after its t2
+// moments (its loads have returned by then); the phase completes when all have, and the slot's
+// next producer waits for that phase
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_complete_tx(uint64_t* b, unsigned tx) {
+  asm volatile("mbarrier.complete_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
 }
 
 // non-blocking phase test
@@ -171,9 +181,7 @@ struct RingIt {
   int it;     // tiles of this CTA before `tile`
   int z;      // slice of the tile
   int gz;     // slices of this CTA before the tile
-  int slotb;  // ring slot of the tile's slice 0 and the parity of its use of that slot
-  int parb;
-  int rsb;    // rows of this CTA before the tile
+  int slotb;  // ring slot of the tile's slice 0
 };
 
 // cp.async copies of slice z of a tile (all its t1 lines) into a staging slot, lanes over unknowns
@@ -400,8 +408,8 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   constexpr int L = ORDER == 2 ? 3 : 5, D = ORDER + 1, NP = D * (D + 1) / 2, NM = ORDER == 2 ? 10 : 20;
   extern __shared__ __align__(16) double smem_rg[];
   __shared__ RingHdr Hs[RG_NH];
-  __shared__ __align__(8) uint64_t bar_row[RG_RR], bar_hdr[RG_NH];
-  __shared__ int ready[RG_RMAX], lastrow[RG_RMAX];
+  __shared__ __align__(8) uint64_t bar_free[RG_RMAX], bar_hdr[RG_NH];
+  __shared__ int ready[RG_RMAX];
 
   const int G1n = op.G1;
   int4* const sgrp = reinterpret_cast<int4*>(smem_rg);
@@ -414,7 +422,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   for (int i = threadIdx.x; i < G1n * 12; i += RG_NTH) stab[i] = __ldg(op.synth1 + i);
   if (threadIdx.x == 0) {
     for (int i = 0; i < RG_RMAX; ++i) ready[i] = 0;
-    for (int i = 0; i < RG_RR; ++i) mbar_init(&bar_row[i], NB);
+    for (int i = 0; i < RG_RMAX; ++i) mbar_init(&bar_free[i], 1);
     for (int i = 0; i < RG_NH; ++i) mbar_init(&bar_hdr[i], 1);
     mbar_fence_init();
   }
@@ -440,8 +448,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         I.z -= H.nz;
         I.gz += H.nz;
         I.slotb += H.nz;
-        if (I.slotb >= R) I.slotb -= R, I.parb ^= 1;
-        I.rsb += H.n2;
+        if (I.slotb >= R) I.slotb -= R;
         I.tile += step;
         ++I.it;
         if (lead && I.tile < n_tiles) {
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
     };
     // P: the slice being projected, F: the next own slice (its copies are in flight), G: the own
     // slice RG_PFD ahead of P, whose lines are being pulled into L2
-    RingIt G{t0, 0, warp, 0, 0, 0, 0};
+    RingIt G{t0, 0, warp, 0, 0};
     if (t0 < n_tiles) rg_wait(&bar_hdr[0], 0);
     settle(G, true);
     RingIt P = G;
@@ -489,13 +496,13 @@ __global__ void __launch_bounds__(RG_NTH, 1)
       int s = P.slotb + P.z;
       if (s >= R) s -= R;
       const int gz = P.gz + P.z;
+      // the slot's previous slice (R slices back, the slot's use number gz / R - 1) has been read
+      // by every block that needs it
+      // (first make sure that slice has been published: its producer may be another, slower A
+      //  warp, and a phase wait one phase early would pass)
       if (gz >= R) {
-        // the slot's previous slice was produced long ago (its rows ran): the fence makes its
-        // lastrow entry visible, then wait until every row that uses it has been read
-        while (lds_acquire(&ready[s]) != gz - R + 1) {
-        }
-        const int need = lastrow[s];
-        rg_wait_relaxed(&bar_row[need & (RG_RR - 1)], (need / RG_RR) & 1);
+        while (lds_acquire(&ready[s]) != gz - R + 1) __nanosleep(100);
+        rg_wait_relaxed(&bar_free[s], (gz / R - 1) & 1);
       }
 #if RG_DIRECT
       if (lane < H.cn) {
@@ -508,13 +515,15 @@ __global__ void __launch_bounds__(RG_NTH, 1)
       if (lane < H.cn)
         ring_phase_a_any<L, D>(H.ny, mybox + (k & 1) * boxd + lane * bpitch, tr0 + s * trd + lane * tpitch, chk);
 #endif
-      // last row of the tile whose t2 window holds this slice
-      int lr = 0;
-      for (int r = 1; r < H.n2; ++r)
-        if (sgrp[H.g2 + r].x - H.z0 <= P.z) lr = r;
+      // blocks that will read this slice: the part's blocks in every row whose window holds it
+      int readers = 0;
+      for (int r = 0; r < H.n2; ++r) {
+        const int w = sgrp[H.g2 + r].x - H.z0;
+        readers += (w <= P.z && P.z < w + L) ? H.n1 : 0;
+      }
       __syncwarp();
       if (lane == 0) {
-        lastrow[s] = P.rsb + lr;
+        mbar_arrive_expect(&bar_free[s], readers);
         __threadfence_block();
         sts_volatile(&ready[s], gz + 1);
       }
@@ -538,30 +547,23 @@ __global__ void __launch_bounds__(RG_NTH, 1)
 #endif
     raise_flag(flag, !isfinite(chk));
   } else {
-    // ============ B warps: blocks round-robin, rows in order ============
+    // ============ B warps: the CTA's blocks round-robin ============
     const int bw = warp - NA;
-    int rs = 0, seq = 0, slotb = 0, gzb = 0, it = 0;
+    int seq = 0, slotb = 0, gzb = 0, it = 0;
     for (int64_t tile = t0; tile < n_tiles; tile += step, ++it) {
       rg_wait(&bar_hdr[it & (RG_NH - 1)], (it / RG_NH) & 1);
       const RingHdr& H = Hs[it & (RG_NH - 1)];
-      const int n1 = H.n1, n2 = H.n2;
+      const int n1 = H.n1, nblk = n1 * H.n2, hg1 = H.g1, hg2 = H.g2, z0 = H.z0, y0 = H.y0;
+      const bool active = lane < H.cn;
+      int i = bw - seq;
+      if (i < 0) i += NB;
+      seq = (seq + nblk) % NB;
 #pragma unroll 1
-      for (int r = 0; r < n2; ++r, ++rs) {
-        int b1 = bw - seq;
-        if (b1 < 0) b1 += NB;
-        seq += n1;
-        if (seq >= NB) seq -= NB;
-        // a warp arrives at the rows in order and never more than 24 rows ahead of the slowest
-        // B warp (the row barriers are reused every RG_RR = 32 rows)
-        if ((rs & 7) == 0 && rs >= 16) rg_wait(&bar_row[(rs - 16) & (RG_RR - 1)], ((rs - 16) / RG_RR) & 1);
-        if (b1 >= n1) {
-          if (lane == 0) mbar_arrive(&bar_row[rs & (RG_RR - 1)]);
-          continue;
-        }
-        const int4 G2 = sgrp[H.g2 + r];
-        const int dz = G2.x - H.z0;
-        const int g1 = H.g1 + b1, g2 = H.g2 + r;
-        const int4 G1 = sgrp[g1];
+      for (; i < nblk; i += NB) {
+        const int r = i / n1, b1 = i - r * n1;
+        const int g1 = hg1 + b1, g2 = hg2 + r;
+        const int4 G1 = sgrp[g1], G2 = sgrp[g2];
+        const int dz = G2.x - z0;
         int zo[L], sl[L];
 #pragma unroll
         for (int j = 0; j < L; ++j) {
@@ -577,11 +579,13 @@ __global__ void __launch_bounds__(RG_NTH, 1)
           for (int j = 0; j < L; ++j) ok &= lds_acquire(&ready[sl[j]]) == gzb + dz + j + 1;
           if (ok) break;
         }
-        const bool active = lane < H.cn;
         double M[NM];
-        if (active) ring_moments<L, D>(tr0 + lane * tpitch + (G1.x - H.y0) * NP, zo, M);
+        if (active) ring_moments<L, D>(tr0 + lane * tpitch + (G1.x - y0) * NP, zo, M);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_row[rs & (RG_RR - 1)]);  // the row's slices are read
+        if (lane == 0) {  // this block has read its slices
+#pragma unroll
+          for (int j = 0; j < L; ++j) mbar_complete_tx(&bar_free[sl[j]], 1);
+        }
         if (active) {
           if (H.narrow) ring_block<D, int>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
           else ring_block<D, int64_t>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);

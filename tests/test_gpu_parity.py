@@ -194,6 +194,40 @@ def test_pool_interp_batch(th, scheme, p):
         assert rel(out[f], want) <= TOL, (f, rel(out[f], want))
 
 
+@pytest.mark.parametrize("scheme,p,n_face", (("order3", 17, 900), ("order2", 17, 900), ("order3", 9, 1500),
+                                             ("order2", 9, 1500)))
+def test_pool_interp_long_batch(th, scheme, p, n_face):
+    """Batches long enough that every persistent CTA walks many tiles (148 CTAs, 2-4 tiles per
+    face): the slice ring's slots, their sequence numbers and reader counts are reused tens of
+    times, and the staged tiles run their double buffers in steady state.  Every 7th face plus
+    the last 40 are checked against the oracle; every output value must be written."""
+    import torch
+
+    k, u = 3, 59
+    rng = np.random.default_rng(p * 3 + len(scheme))
+    E = p + 2 * k
+    n_patch = 8
+    pool = rng.standard_normal((n_patch, E ** 3 * u))
+    cid = rng.integers(0, n_patch, n_face)
+    nrm = rng.integers(0, 3, n_face)
+    sid = rng.integers(0, 2, n_face)
+    seg = rng.integers(0, 9, n_face)
+    op = th.operators.DEFAULT_CACHE.device_operator("interpolate", scheme, p, k)
+    batch = th.FaceBatch(op, th.pool_interp_faces(p, k, u, cid, nrm, sid, seg), u)
+    dev = torch.device("cuda")
+    dst = torch.full((n_face * k * p * p * u,), np.nan, dtype=torch.float64, device=dev)
+    batch.launch(torch.from_numpy(pool.reshape(-1)).to(dev), dst)
+    assert not batch.nonfinite()
+    assert bool(torch.isfinite(dst).all())
+    out = dst.cpu().numpy().reshape(n_face, -1)
+    for f in sorted(set(range(0, n_face, 7)) | set(range(n_face - 40, n_face))):
+        lo, ext = _interp_box(p, k, int(nrm[f]), int(sid[f]))
+        box = _world_box(pool, E, u, int(cid[f]), lo, ext)
+        cfg = th.FaceConfig("xyz"[nrm[f]], ("negative", "positive")[sid[f]], int(seg[f]), p, k, u)
+        want = oracle_run(cfg, scheme, "interpolate", None, box)
+        assert rel(out[f], want) <= TOL, (f, rel(out[f], want))
+
+
 @pytest.mark.parametrize("u", (1, 33, 65, 130, 200))
 @pytest.mark.parametrize("scheme,p", (("tensor_linear", 9), ("order2", 9), ("order3", 9), ("order2", 17)))
 def test_pool_interp_unknown_counts(th, scheme, p, u):
@@ -372,7 +406,8 @@ def test_alternative_kernel_paths(th, env):
     here = os.path.dirname(os.path.abspath(__file__))
     res = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_parity.py"),
-         "-k", "exchange_all_faces_small or pool_interp_batch or pool_restrict_batch or transposed or unknown_counts"],
+         "-k", "exchange_all_faces_small or pool_interp_batch or pool_interp_long_batch or pool_restrict_batch or transposed "
+         "or unknown_counts"],
         env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
 
