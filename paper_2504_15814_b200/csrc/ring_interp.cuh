@@ -130,30 +130,40 @@ struct RingHdr {
   int4 G0;             // the normal group
 };
 
-// tile = ((face, t1 part), chunk)
+// tile = ((face, t1 part), chunk).  One thread decodes a tile; every field of the face record
+// is loaded unconditionally (one global-memory latency instead of decode_face's record ->
+// stride -> group chain) and the group table is read from its shared-memory copy.
 template <int L>
 __device__ __forceinline__ void ring_decode(const DevOp& op, const th_face* __restrict__ faces, int64_t tile,
-                                            int ntp, int nch, int u, RingHdr& H) {
+                                            int ntp, int nch, int u, const int4* sgrp, int4 G0, RingHdr& H) {
   const int64_t st = tile / nch;
   const int c = int(tile - st * nch);
   const int64_t f = st / ntp;
   const int tp = int(st - f * ntp);
-  FaceRef fr;
-  decode_face(faces + f, op, fr);
-  const int a1 = tp * fr.n1 / ntp, b1 = (tp + 1) * fr.n1 / ntp;
-  H.g1 = fr.g1 + a1;
+  const th_face* const fp = faces + f;
+  const int64_t src0 = __ldg(&fp->src[0]), dst0 = __ldg(&fp->dst);
+  const int64_t ss0 = __ldg(&fp->src_stride[0]), ss1 = __ldg(&fp->src_stride[1]), ss2 = __ldg(&fp->src_stride[2]);
+  const int64_t ds0 = __ldg(&fp->dst_stride[0]), ds1 = __ldg(&fp->dst_stride[1]), ds2 = __ldg(&fp->dst_stride[2]);
+  const int n = __ldg(&fp->normal), side = __ldg(&fp->side), seg = __ldg(&fp->segment);
+  // reference frame (decode_face, role 0): normal n, tangentials t1 < t2; the normal flip of
+  // geometry.py:180-190 folded into the signed strides
+  const int64_t ssn = n == 0 ? ss0 : n == 1 ? ss1 : ss2, dsn = n == 0 ? ds0 : n == 1 ? ds1 : ds2;
+  H.s1 = n == 0 ? ss1 : ss0;
+  H.s2 = n == 2 ? ss1 : ss2;
+  H.d1 = n == 0 ? ds1 : ds0;
+  H.d2 = n == 2 ? ds1 : ds2;
+  H.sn = side ? -ssn : ssn;
+  H.dn = side ? -dsn : dsn;
+  H.dst_off = dst0 + (side ? int64_t(op.k - 1) * dsn : 0);
+  const int c1 = seg % 3, c2 = seg / 3;
+  H.lo1 = c1 * op.p;
+  H.lo2 = c2 * op.p;
+  const int fg1 = op.seg_g[c1][0], fn1 = op.seg_g[c1][1] - fg1;
+  const int a1 = tp * fn1 / ntp, b1 = (tp + 1) * fn1 / ntp;
+  H.g1 = fg1 + a1;
   H.n1 = b1 - a1;
-  H.g2 = fr.g2;
-  H.n2 = fr.n2;
-  H.dst_off = fr.dst;
-  H.sn = fr.sn;
-  H.s1 = fr.s1;
-  H.s2 = fr.s2;
-  H.dn = fr.dn;
-  H.d1 = fr.d1;
-  H.d2 = fr.d2;
-  H.lo1 = fr.lo1;
-  H.lo2 = fr.lo2;
+  H.g2 = op.seg_g[c2][0];
+  H.n2 = op.seg_g[c2][1] - H.g2;
   H.cb = int(int64_t(c) * u / nch);
   H.cn = int(int64_t(c + 1) * u / nch) - H.cb;
   if (H.n1 <= 0 || H.n2 <= 0 || H.cn <= 0) {  // empty tile: no slices, no rows
@@ -161,18 +171,18 @@ __device__ __forceinline__ void ring_decode(const DevOp& op, const th_face* __re
     H.y0 = H.z0 = H.ny = H.nz = 0;
     H.cn = 0;
   } else {
-    H.y0 = __ldg(&op.grp1[H.g1]).x;
-    H.ny = __ldg(&op.grp1[H.g1 + H.n1 - 1]).x + L - H.y0;
-    H.z0 = __ldg(&op.grp1[H.g2]).x;
-    H.nz = __ldg(&op.grp1[H.g2 + H.n2 - 1]).x + L - H.z0;
+    H.y0 = sgrp[H.g1].x;
+    H.ny = sgrp[H.g1 + H.n1 - 1].x + L - H.y0;
+    H.z0 = sgrp[H.g2].x;
+    H.nz = sgrp[H.g2 + H.n2 - 1].x + L - H.z0;
   }
-  const int4 G0 = __ldg(&op.grp0[fr.g0]);
   H.G0 = G0;
-  H.src_off = fr.src0 + int64_t(G0.x) * fr.sn + int64_t(H.y0) * fr.s1 + int64_t(H.z0) * fr.s2 + H.cb;
+  H.src_off = src0 + (side ? int64_t(op.ns0 - 1) * ssn : 0) + int64_t(G0.x) * H.sn + int64_t(H.y0) * H.s1 +
+              int64_t(H.z0) * H.s2 + H.cb;
   const int64_t lim = int64_t(1) << 21;
   auto small = [lim](int64_t s) { return s > -lim && s < lim; };
-  H.narrow = small(fr.dn) && small(fr.d1) && small(fr.d2) && op.p <= 64 && u <= (1 << 20);
-  H.snarrow = small(fr.sn) && small(fr.s1) && op.p <= 64;
+  H.narrow = small(H.dn) && small(H.d1) && small(H.d2) && op.p <= 64 && u <= (1 << 20);
+  H.snarrow = small(H.sn) && small(H.s1) && op.p <= 64;
 }
 
 // position of an A warp in the CTA's slice stream: slice z of the it-th tile of the CTA
@@ -429,18 +439,21 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t0 = blockIdx.x, step = gridDim.x;
+  const int4 G0c = __ldg(&op.grp0[0]);  // the single normal group (prepare_ring)
 
   if (warp < NA) {
     // ============ A warps: fetch, phase A of every NA-th slice ============
-    const bool scout = warp == 0 && lane == 0;  // decodes the tile headers
-    if (scout)
-      for (int i = 0; i < RG_HAHEAD; ++i)
+    // tile headers are decoded RG_HAHEAD tiles ahead, tile i by lane 0 of A warp i mod NA (one
+    // warp decoding them all falls a decode -- two dependent global loads -- per tile behind the
+    // others, and every block needs slices of every A warp)
+    if (lane == 0)
+      for (int i = warp; i < RG_HAHEAD; i += NA)
         if (t0 + i * step < n_tiles) {
-          ring_decode<L>(op, faces, t0 + i * step, ntp, nch, u, Hs[i]);
+          ring_decode<L>(op, faces, t0 + i * step, ntp, nch, u, sgrp, G0c, Hs[i]);
           mbar_arrive(&bar_hdr[i]);
         }
     // move an iterator whose z ran past its tile to the tile holding that slice; the leading
-    // iterator waits for (and the scout decodes) headers, the others follow it
+    // iterator waits for headers (and decodes its share of them), the others follow it
     auto settle = [&](RingIt& I, bool lead) {
       while (I.tile < n_tiles) {
         const RingHdr& H = Hs[I.it & (RG_NH - 1)];
@@ -454,8 +467,8 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         if (lead && I.tile < n_tiles) {
           const int64_t nt = I.tile + int64_t(RG_HAHEAD - 1) * step;
           const int ni = I.it + RG_HAHEAD - 1;
-          if (scout && nt < n_tiles) {
-            ring_decode<L>(op, faces, nt, ntp, nch, u, Hs[ni & (RG_NH - 1)]);
+          if (lane == 0 && ni % NA == warp && nt < n_tiles) {
+            ring_decode<L>(op, faces, nt, ntp, nch, u, sgrp, G0c, Hs[ni & (RG_NH - 1)]);
             mbar_arrive(&bar_hdr[ni & (RG_NH - 1)]);
           }
           __syncwarp();

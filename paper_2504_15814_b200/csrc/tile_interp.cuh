@@ -65,14 +65,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // one thread: decode tile `tile` of the launch
+// (grp: the tangential group table, its shared-memory copy once that is filled)
 __device__ __forceinline__ void tile_decode(const DevOp& op, const th_face* __restrict__ faces, int64_t tile, int nt,
-                                            int u, TileHdr& H) {
+                                            int u, TileHdr& H, const int4* grp) {
   const int64_t tpf = int64_t(nt) * nt;
   const int64_t f = tile / tpf;
   const int tt = int(tile - f * tpf);
   const int ti2 = tt / nt, ti1 = tt - ti2 * nt;
   FaceRef fr;
-  decode_face(faces + f, op, fr);
+  decode_face_interp(faces + f, op, fr);
   const int a1 = ti1 * fr.n1 / nt, b1 = (ti1 + 1) * fr.n1 / nt;
   const int a2 = ti2 * fr.n2 / nt, b2 = (ti2 + 1) * fr.n2 / nt;
   H.g0 = fr.g0;
@@ -95,10 +96,10 @@ __device__ __forceinline__ void tile_decode(const DevOp& op, const th_face* __re
     H.ny = H.nz = 0;
     H.cnt = 0;
   } else {
-    H.y0 = __ldg(&op.grp1[H.g1]).x;
-    H.ny = __ldg(&op.grp1[H.g1 + H.n1 - 1]).x + 3 - H.y0;
-    H.z0 = __ldg(&op.grp1[H.g2]).x;
-    H.nz = __ldg(&op.grp1[H.g2 + H.n2 - 1]).x + 3 - H.z0;
+    H.y0 = grp[H.g1].x;
+    H.ny = grp[H.g1 + H.n1 - 1].x + 3 - H.y0;
+    H.z0 = grp[H.g2].x;
+    H.nz = grp[H.g2 + H.n2 - 1].x + 3 - H.z0;
     H.cnt = H.n1 * H.n2 * u;
   }
   const int4 G0 = __ldg(&op.grp0[fr.g0]);
@@ -351,9 +352,10 @@ __global__ void __launch_bounds__(NTH, MINB)
   constexpr int DEC = NTH - 1;
   const int64_t t0 = blockIdx.x, step = gridDim.x;
   const bool pf = op.prefetch & 16;  // TH_PREFETCH bit 16: L2 prefetch of the tile after next
+  __syncthreads();  // tables filled: the decodes read the group table from shared memory
   if (threadIdx.x == DEC)
     for (int i = 0; i < 3; ++i)
-      if (t0 + i * step < n_tiles) tile_decode(op, faces, t0 + i * step, nt, u, Hs[i]);
+      if (t0 + i * step < n_tiles) tile_decode(op, faces, t0 + i * step, nt, u, Hs[i], sgrp);
   __syncthreads();
   if (t0 < n_tiles) tile_fetch<NTH>(Hs[0], src, boxes, pitch, u);
   cp_async_commit();
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     if (tile + step < n_tiles) tile_fetch<NTH>(Hs[(it + 1) & 3], src, boxes + ((it + 1) & 1) * box_doubles, pitch, u);
     cp_async_commit();
     if (pf && tile + 2 * step < n_tiles) tile_prefetch_l2<NTH>(Hs[(it + 2) & 3], src, u);
-    if (threadIdx.x == DEC && tile + 3 * step < n_tiles) tile_decode(op, faces, tile + 3 * step, nt, u, Hs[(it + 3) & 3]);
+    if (threadIdx.x == DEC && tile + 3 * step < n_tiles) tile_decode(op, faces, tile + 3 * step, nt, u, Hs[(it + 3) & 3], sgrp);
     const TileHdr& H = Hs[it & 3];
     const double* box = boxes + (it & 1) * box_doubles;
     if (H.narrow) tile_compute<TENSOR, NTH, int>(H, op, dst, box, pitch, stab, stab0, sgrp, u, umag, chk);

@@ -62,14 +62,14 @@ __device__ __forceinline__ int tile3_bound(int c, int nch, int u, int align) {
 // tile = ((face, t2 tile, t1 tile), chunk): a face splits into nt x nt spatial tiles of <= 3 x 3
 // blocks (nt = 1 at p <= 9) and every spatial tile into nch chunks of unknowns
 __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __restrict__ faces, int64_t tile,
-                                             int nt, int nch, int align, int u, Tile3Hdr& H) {
+                                             int nt, int nch, int align, int u, Tile3Hdr& H, const int4* grp) {
   const int64_t st = tile / nch;
   const int c = int(tile - st * nch);
   const int64_t f = st / (nt * nt);
   const int tt = int(st - f * (nt * nt));
   const int ti2 = tt / nt, ti1 = tt - ti2 * nt;
   FaceRef fr;
-  decode_face(faces + f, op, fr);
+  decode_face_interp(faces + f, op, fr);
   const int a1 = ti1 * fr.n1 / nt, b1 = (ti1 + 1) * fr.n1 / nt;
   const int a2 = ti2 * fr.n2 / nt, b2 = (ti2 + 1) * fr.n2 / nt;
   H.g0 = fr.g0;
@@ -94,12 +94,12 @@ __device__ __forceinline__ void tile3_decode(const DevOp& op, const th_face* __r
     H.ny = H.nz = 0;
     H.cn = 0;
   } else {
-    H.y0 = __ldg(&op.grp1[H.g1]).x;
-    H.ny = __ldg(&op.grp1[H.g1 + H.n1 - 1]).x + 5 - H.y0;
-    H.z0 = __ldg(&op.grp1[H.g2]).x;
-    H.nz = __ldg(&op.grp1[H.g2 + H.n2 - 1]).x + 5 - H.z0;
+    H.y0 = grp[H.g1].x;
+    H.ny = grp[H.g1 + H.n1 - 1].x + 5 - H.y0;
+    H.z0 = grp[H.g2].x;
+    H.nz = grp[H.g2 + H.n2 - 1].x + 5 - H.z0;
   }
-  const int4 G0 = __ldg(&op.grp0[fr.g0]);
+  const int4 G0 = __ldg(&op.grp0[0]);  // the single normal group (prepare_tile3)
   H.G0 = G0;
   H.src_off = fr.src0 + int64_t(G0.x) * fr.sn + int64_t(H.y0) * fr.s1 + int64_t(H.z0) * fr.s2 + H.cb;
   H.n1mag = recip16(H.n1);
@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(T3P_NTH, 1)
   // named barriers: T_FULL[k] = 1 + k, T_EMPTY[k] = 1 + NT + k (bar.arrive by the producing
   // group, bar.sync by the consuming group; counts include both groups)
   static_assert(2 * NT + 1 <= 16 && NT + 5 <= 8 + 1, "named barriers / header ring");
+  __syncthreads();  // tables filled: the header decodes read the group table from shared memory
   if (warp < NA3) {
     // ============ A warps: fetch, phase A ============
     // A warp w owns box slice z = w (NA3 == T3Y): it fetches that slice of every tile and takes
@@ -471,9 +472,11 @@ __global__ void __launch_bounds__(T3P_NTH, 1)
     // so the A warps need no barrier among themselves.
     static_assert(NA3 == T3Y, "one A warp per t2 slice of the box");
     const int atid = threadIdx.x;
-    if (atid == 0)
-      for (int i = 0; i < 5; ++i)
-        if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nt, nch, align, u, Hs[i]);
+    // tile headers are decoded 5 tiles ahead, tile i by lane 0 of A warp i mod NA3 (a warp that
+    // decoded them all would reach every hand-off a global-memory latency after the others)
+    if ((atid & 31) == 0)
+      for (int i = warp; i < 5; i += NA3)
+        if (t0 + i * step < n_tiles) tile3_decode(op, faces, t0 + i * step, nt, nch, align, u, Hs[i], sgrp);
     __syncthreads();  // (with the B warps: tables and headers 0..4 visible to everyone)
     for (int i = 0; i < NBX; ++i) {
       if (t0 + i * step < n_tiles) tile3_fetch_slice(Hs[i], src, box0 + i * boxd, warp);
@@ -487,8 +490,8 @@ __global__ void __launch_bounds__(T3P_NTH, 1)
       if constexpr (NBX == 1) cp_async_wait_all();   // this thread's slice of tile `it` landed
       else cp_async_wait_one();
       if (it >= NT) bar_sync_n(1 + NT + tb, ALL);     // B is done with T[tb] (tile it - NT)
-      if (atid == 0 && tile + 5 * step < n_tiles)     // Hs[(it + 5) & 7]: B is past tile it - NT
-        tile3_decode(op, faces, tile + 5 * step, nt, nch, align, u, Hs[(it + 5) & 7]);
+      if ((atid & 31) == 0 && (it + 5) % NA3 == warp && tile + 5 * step < n_tiles)  // B is past tile it - NT
+        tile3_decode(op, faces, tile + 5 * step, nt, nch, align, u, Hs[(it + 5) & 7], sgrp);
       const Tile3Hdr& H = Hs[it & 7];
       if (warp < H.nz && (threadIdx.x & 31) < H.cn) {
         double* const bxp = box0 + bx * boxd;
