@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         I.z -= H.nz;
         I.gz += H.nz;
         I.slotb += H.nz;
-        if (I.slotb >= R) I.slotb -= R;
+        while (I.slotb >= R) I.slotb -= R;  // (a tile may hold more slices than the ring)
         I.tile += step;
         ++I.it;
         if (lead && I.tile < n_tiles) {
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
 #endif
       const RingHdr& H = Hs[P.it & (RG_NH - 1)];
       int s = P.slotb + P.z;
-      if (s >= R) s -= R;
+      while (s >= R) s -= R;
       const int gz = P.gz + P.z;
       // the slot's previous slice (R slices back, the slot's use number gz / R - 1) has been read
       // by every block that needs it
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
 #pragma unroll
         for (int j = 0; j < L; ++j) {
           int s = slotb + dz + j;
-          if (s >= R) s -= R;
+          while (s >= R) s -= R;
           sl[j] = s;
           zo[j] = s * trd;
         }
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         }
       }
       slotb += H.nz;
-      if (slotb >= R) slotb -= R;
+      while (slotb >= R) slotb -= R;
       gzb += H.nz;
     }
   }
