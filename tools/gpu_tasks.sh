@@ -26,6 +26,11 @@ for task in "$@"; do
                 timeout 600 $cmd8 > gpurun_out/ncu_plain8.json 2>&1 &&
                 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"tile3p|stage_slide" -s 2 -c 2 -o gpurun_out/prof_c5 -f $cmd8 > gpurun_out/ncu_full.log 2>&1
                 tail -2 gpurun_out/ncu_full.log ;;
+    ncu_cfg[1-4]) # launch list + one full-set capture of every interpolation / restriction kernel of config N
+                n=${task#ncu_cfg}; cmd="python bench.py --config $n --steps 1 --warmup 1 --no-e2e --no-cpu --no-same-level"
+                timeout 600 $cmd > gpurun_out/ncu_plain_c$n.json 2> gpurun_out/ncu_plain_c$n.err &&
+                timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"ring_interp|tile3p|tile_interp|stage_slide|restrict_reg|gram_slide" -s $(( n == 3 ? 4 : 8 )) -c 4 -o gpurun_out/prof_c$n -f $cmd > gpurun_out/ncu_full_c$n.log 2>&1
+                tail -2 gpurun_out/ncu_full_c$n.log ;;
     reftests)   # the reference's own tests against the drop-in (needs baseline/_ref/tests_ref, git-ignored)
                 timeout 1200 python tools/run_reference_tests.py baseline/_ref/tests_ref test_schemes.py -q > gpurun_out/reftests_schemes.log 2>&1; tail -3 gpurun_out/reftests_schemes.log
                 timeout 1800 python tools/run_reference_tests.py baseline/_ref/tests_ref test_acceptance.py -q -k "criterion_1 or criterion_2 or criterion_3 or criterion_4" > gpurun_out/reftests_acceptance.log 2>&1; tail -3 gpurun_out/reftests_acceptance.log

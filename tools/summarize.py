@@ -16,7 +16,7 @@ import sys
 from collections import OrderedDict
 
 
-OURS = ("strided_box_kernel", "box_copy_kernel", "restrict_reg_kernel", "gram_slide_kernel", "tile_interp_kernel", "tile3_interp_kernel", "tile3p_interp_kernel", "stage_slide_kernel", "window_kernel", "dense_apply_kernel",
+OURS = ("ring_interp_kernel", "strided_box_kernel", "box_copy_kernel", "restrict_reg_kernel", "gram_slide_kernel", "tile_interp_kernel", "tile3_interp_kernel", "tile3p_interp_kernel", "stage_slide_kernel", "window_kernel", "dense_apply_kernel",
         "tensor_apply_kernel", "finite_kernel", "csr_apply_kernel")
 SCALE = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6,
          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
