@@ -47,16 +47,19 @@ struct Tile {
 
 // tile ti of a face: t1 groups [gA, gB) of the face's range, their window union
 // [y0, y0 + ny) along t1 and the union [z0, z1) of all its t2 windows
-__device__ __forceinline__ bool tile_of(const DevOp& op, const FaceRef& fr, int ti, int tg, int L, Tile& t) {
+// (grp: the tangential group table, its shared-memory copy in the kernel)
+__device__ __forceinline__ bool tile_of(const int4* grp, const FaceRef& fr, int ti, int tg, int L, Tile& t) {
   t.gA = fr.g1 + ti * tg;
   t.gB = min(fr.g1 + fr.n1, t.gA + tg);
   if (fr.n0 != 1 || t.gA >= t.gB || fr.n2 < 1) return false;
-  t.y0 = __ldg(&op.grp1[t.gA]).x;
-  t.ny = __ldg(&op.grp1[t.gB - 1]).x + L - t.y0;
-  t.z0 = __ldg(&op.grp1[fr.g2]).x;
-  t.z1 = __ldg(&op.grp1[fr.g2 + fr.n2 - 1]).x + L;
+  t.y0 = grp[t.gA].x;
+  t.ny = grp[t.gB - 1].x + L - t.y0;
+  t.z0 = grp[fr.g2].x;
+  t.z1 = grp[fr.g2 + fr.n2 - 1].x + L;
   return true;
 }
+
+constexpr int kGrpSmem = 96;  // tangential groups copied to shared memory (3 p <= 96)
 
 __device__ __forceinline__ int round_even(int v) { return (v + 1) & ~1; }
 
@@ -84,6 +87,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);             // [NST][ny_max]
   unsigned char* const shr = reinterpret_cast<unsigned char*>(eline + NST * ny_max);  // producer scratch
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  // group table and synthesis-row classes in shared memory: a tile's header (face record ->
+  // groups -> classes) then costs one global-memory latency instead of a chain of four, which
+  // every consumer warp used to wait out at the start of each tile while the ring stood full
+  __shared__ int4 sgrp_s[kGrpSmem];
+  __shared__ int scls_s[kGrpSmem];
+  const bool gsm = op.G1 <= kGrpSmem;
+  const int4* const grp = gsm ? sgrp_s : op.grp1;
+  const int* const cls = gsm ? scls_s : op.st_cls;
+  const int4 G0c = __ldg(&op.grp0[0]);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int p = op.p, G1 = op.G1;
@@ -101,6 +113,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     // W_a(y, z) of every (t1, t2) synthesis-row class pair (host-built, trihalo.cu prepare_stage)
     for (int i = threadIdx.x; i < op.st_ncls * op.st_ncls * 100; i += blockDim.x) wtab[i] = __ldg(op.st_w + i);
     for (int i = threadIdx.x; i < 20; i += blockDim.x) wzero[i] = 0.0;
+    if (gsm)
+      for (int i = threadIdx.x; i < op.G1; i += blockDim.x) {
+        sgrp_s[i] = __ldg(&op.grp1[i]);
+        scls_s[i] = __ldg(&op.st_cls[i]);
+      }
   }
   __syncthreads();
 
@@ -111,11 +128,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int64_t f = tile / tiles_per_face;
       const th_face* fp = faces + f;
+      if (tile + gridDim.x < total && lane < 2)  // the next tile's face record (144 bytes) into L2
+        l2_prefetch_line(reinterpret_cast<const char*>(faces + (tile + gridDim.x) / tiles_per_face) + 128 * lane);
       FaceRef fr;
-      decode_face(fp, op, fr);
+      decode_face_restrict(fp, op, fr);
       Tile t;
-      if (!tile_of(op, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
-      const int4 G0 = __ldg(&op.grp0[fr.g0]);
+      if (!tile_of(grp, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
+      const int4 G0 = fr.g0 == 0 ? G0c : __ldg(&op.grp0[fr.g0]);
       const int nx = G0.y, x0 = G0.x;
       const int64_t adj = fr.src0 - __ldg(&fp->src[0]);
       const int mode = (fr.sn == u || fr.sn == -u) ? 0 : (fr.s1 == u ? 1 : 2);
@@ -301,13 +320,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       const int64_t f = tile / tiles_per_face;
       const th_face* fp = faces + f;
       FaceRef fr;
-      decode_face(fp, op, fr);
+      decode_face_restrict(fp, op, fr);
       Tile t;
-      if (!tile_of(op, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
+      if (!tile_of(grp, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
       const bool active = gi < t.gB - t.gA && warp < tg * nch;
       const int g1 = t.gA + (active ? gi : 0);
-      const int ly = __ldg(&op.grp1[g1]).x - t.y0;
-      const double* const wrow = wtab + __ldg(&op.st_cls[g1]) * ncl * 100;  // + c2 * 100 per window
+      const int ly = grp[g1].x - t.y0;
+      const double* const wrow = wtab + cls[g1] * ncl * 100;  // + c2 * 100 per window
       const int cb = chunk * 32 * NU;
       bool ok[NU];
 #pragma unroll
@@ -318,9 +337,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 #pragma unroll
         for (int i = 0; i < D; ++i) UA[q][i] = UB[q][i] = 0.0;
       int j = 0;
-      int wA = __ldg(&op.grp1[0]).x;
-      int wB = G1 > 1 ? __ldg(&op.grp1[1]).x : INT_MAX / 2;
-      int cA = __ldg(&op.st_cls[0]), cB = G1 > 1 ? __ldg(&op.st_cls[1]) : 0;
+      int wA = grp[0].x;
+      int wB = G1 > 1 ? grp[1].x : INT_MAX / 2;
+      int cA = cls[0], cB = G1 > 1 ? cls[1] : 0;
       bool bad = false;
       for (int a2 = t.z0; a2 < t.z1; ++a2) {
         const int zA = a2 - wA, zB = a2 - wB;
@@ -373,9 +392,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
         if (!active) continue;
         if (zA == L - 1) {
           // ---- window j complete: its normal children, store ----
-          const int t1 = __ldg(&op.grp1[g1]).z, t2 = __ldg(&op.grp1[j]).z;
+          const int t1 = grp[g1].z, t2 = grp[j].z;
           if (t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p) {
-            const int4 G0 = __ldg(&op.grp0[fr.g0]);
+            const int4 G0 = fr.g0 == 0 ? G0c : __ldg(&op.grp0[fr.g0]);
             const double* s0 = op.synth0 + fr.g0 * 12;
             double* const ob = dst + fr.dst + int64_t(t1 - fr.lo1) * fr.d1 + int64_t(t2 - fr.lo2) * fr.d2 + cb + lane;
 #pragma unroll
@@ -408,8 +427,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
           ++j;
           wA = wB;
           cA = cB;
-          wB = j + 1 < G1 ? __ldg(&op.grp1[j + 1]).x : INT_MAX / 2;
-          cB = j + 1 < G1 ? __ldg(&op.st_cls[j + 1]) : 0;
+          wB = j + 1 < G1 ? grp[j + 1].x : INT_MAX / 2;
+          cB = j + 1 < G1 ? cls[j + 1] : 0;
         }
       }
       if (active) raise_flag(flag, bad);

@@ -160,6 +160,30 @@ __device__ __forceinline__ void decode_face_interp(const th_face* __restrict__ f
   r.n2 = op.seg_g[s / 3][1] - r.g2;
 }
 
+// decode_face for restriction faces (role 1), every field loaded unconditionally (one latency)
+__device__ __forceinline__ void decode_face_restrict(const th_face* __restrict__ fp, const DevOp& op, FaceRef& r) {
+  const int64_t src0 = __ldg(&fp->src[0]), dst0 = __ldg(&fp->dst);
+  const int64_t ss0 = __ldg(&fp->src_stride[0]), ss1 = __ldg(&fp->src_stride[1]), ss2 = __ldg(&fp->src_stride[2]);
+  const int64_t ds0 = __ldg(&fp->dst_stride[0]), ds1 = __ldg(&fp->dst_stride[1]), ds2 = __ldg(&fp->dst_stride[2]);
+  const int n = __ldg(&fp->normal), side = __ldg(&fp->side), h = __ldg(&fp->half);
+  const int64_t ssn = n == 0 ? ss0 : n == 1 ? ss1 : ss2, dsn = n == 0 ? ds0 : n == 1 ? ds1 : ds2;
+  r.s1 = n == 0 ? ss1 : ss0;
+  r.s2 = n == 2 ? ss1 : ss2;
+  r.d1 = n == 0 ? ds1 : ds0;
+  r.d2 = n == 2 ? ds1 : ds2;
+  r.sn = side ? -ssn : ssn;
+  r.dn = side ? -dsn : dsn;
+  r.src0 = src0 + (side ? int64_t(op.ns0 - 1) * ssn : 0);
+  r.lo0 = op.half_t[h][0];
+  r.hi0 = op.half_t[h][1];
+  r.lo1 = r.lo2 = 0;
+  r.g0 = op.half_g[h][0];
+  r.n0 = op.half_g[h][1] - r.g0;
+  r.g1 = r.g2 = 0;
+  r.n1 = r.n2 = op.G1;
+  r.dst = dst0 + (side ? int64_t(r.hi0 - r.lo0 - 1) * dsn : 0);
+}
+
 // source address of reference source cell (a0, a1, a2) (relative to lane 0)
 __device__ __forceinline__ int64_t src_addr(const th_face* __restrict__ fp, const DevOp& op, const FaceRef& r,
                                             int a0, int a1, int a2) {
