@@ -570,10 +570,13 @@ __global__ void __launch_bounds__(RG_NTH, 1)
       const bool active = lane < H.cn;
       int i = bw - seq;
       if (i < 0) i += NB;
-      seq = (seq + nblk) % NB;
+      seq += nblk;  // (mod NB by subtraction: nblk <= 28, no integer division)
+      while (seq >= NB) seq -= NB;
 #pragma unroll 1
       for (; i < nblk; i += NB) {
-        const int r = i / n1, b1 = i - r * n1;
+        // i / n1 for n1 <= 4, i < 32 (n1 = 3: 11 i >> 5 is exact up to i = 31)
+        const int r = n1 == 3 ? (i * 11) >> 5 : n1 == 4 ? i >> 2 : n1 == 2 ? i >> 1 : i;
+        const int b1 = i - r * n1;
         const int g1 = hg1 + b1, g2 = hg2 + r;
         const int4 G1 = sgrp[g1], G2 = sgrp[g2];
         const int dz = G2.x - z0;
