@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128, MINB) restrict_reg_kernel(DevOp op,
     const int64_t f = item / op.max_items;
     const th_face* fp = faces + f;
     FaceRef fr;
-    decode_face(fp, op, fr);
+    decode_face_restrict(fp, op, fr);
     int g0, g1, g2;
     if (!decode_item(op, fr, int(item - f * op.max_items), g0, g1, g2)) continue;
     const int4 G0 = __ldg(&op.grp0[g0]), G1 = __ldg(&op.grp1[g1]), G2 = __ldg(&op.grp1[g2]);

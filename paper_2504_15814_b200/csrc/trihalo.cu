@@ -88,52 +88,12 @@ struct FaceRef {
   int g0, n0, g1, n1, g2, n2;
 };
 
-__device__ __forceinline__ void decode_face(const th_face* __restrict__ fp, const DevOp& op, FaceRef& r) {
-  const int n = __ldg(&fp->normal);
-  const int side = __ldg(&fp->side);
-  const int t1 = (n == 0) ? 1 : 0, t2 = (n == 2) ? 1 : 2;
-  const int64_t ssn = __ldg(&fp->src_stride[n]);
-  r.s1 = __ldg(&fp->src_stride[t1]);
-  r.s2 = __ldg(&fp->src_stride[t2]);
-  r.sn = side ? -ssn : ssn;
-  const int64_t sadj = side ? int64_t(op.ns0 - 1) * ssn : 0;
-  r.src0 = __ldg(&fp->src[0]) + sadj;
-  const int64_t dsn = __ldg(&fp->dst_stride[n]);
-  r.d1 = __ldg(&fp->dst_stride[t1]);
-  r.d2 = __ldg(&fp->dst_stride[t2]);
-  int box0;
-  if (op.role == 0) {
-    const int s = __ldg(&fp->segment);
-    r.lo0 = 0;
-    r.hi0 = op.k;
-    r.lo1 = (s % 3) * op.p;
-    r.lo2 = (s / 3) * op.p;
-    r.g0 = 0;
-    r.n0 = op.G0;
-    r.g1 = op.seg_g[s % 3][0];
-    r.n1 = op.seg_g[s % 3][1] - r.g1;
-    r.g2 = op.seg_g[s / 3][0];
-    r.n2 = op.seg_g[s / 3][1] - r.g2;
-    box0 = op.k;
-  } else {
-    const int h = __ldg(&fp->half);
-    r.lo0 = op.half_t[h][0];
-    r.hi0 = op.half_t[h][1];
-    r.lo1 = r.lo2 = 0;
-    r.g0 = op.half_g[h][0];
-    r.n0 = op.half_g[h][1] - r.g0;
-    r.g1 = r.g2 = 0;
-    r.n1 = r.n2 = op.G1;
-    box0 = r.hi0 - r.lo0;
-  }
-  r.dn = side ? -dsn : dsn;
-  r.dst = __ldg(&fp->dst) + (side ? int64_t(box0 - 1) * dsn : 0);
-}
-
-// decode_face for interpolation faces (role 0) with every field of the record loaded
-// unconditionally: one global-memory latency instead of the record -> stride chain.  The
-// persistent tile kernels decode a tile per iteration on one thread, whose warp the others
-// wait for.
+// Every field of the record is loaded unconditionally and the axis-dependent ones selected
+// afterwards: one global-memory latency per decode (loading normal / side first and then the
+// strides they select is a chain of dependent loads, which the persistent tile kernels -- one
+// decoding thread per tile, whose warp the others wait for -- and the per-warp restriction
+// kernel had on their critical paths; profiles/r02_ab_ring.txt).
+// interpolation faces (role 0):
 __device__ __forceinline__ void decode_face_interp(const th_face* __restrict__ fp, const DevOp& op, FaceRef& r) {
   const int64_t src0 = __ldg(&fp->src[0]), dst0 = __ldg(&fp->dst);
   const int64_t ss0 = __ldg(&fp->src_stride[0]), ss1 = __ldg(&fp->src_stride[1]), ss2 = __ldg(&fp->src_stride[2]);
@@ -182,6 +142,11 @@ __device__ __forceinline__ void decode_face_restrict(const th_face* __restrict__
   r.g1 = r.g2 = 0;
   r.n1 = r.n2 = op.G1;
   r.dst = dst0 + (side ? int64_t(r.hi0 - r.lo0 - 1) * dsn : 0);
+}
+
+__device__ __forceinline__ void decode_face(const th_face* __restrict__ fp, const DevOp& op, FaceRef& r) {
+  if (op.role == 0) decode_face_interp(fp, op, r);
+  else decode_face_restrict(fp, op, r);
 }
 
 // source address of reference source cell (a0, a1, a2) (relative to lane 0)
