@@ -200,14 +200,24 @@ __device__ __forceinline__ void ring_fetch(const RingHdr& H, const double* __res
                                            int z) {
   const int lane = threadIdx.x & 31;
   if (lane >= H.cn) return;
-  const int64_t sn = H.sn, s1 = H.s1;
   const double* const base = src + (H.src_off + lane + int64_t(z) * H.s2);
   double* const bq = bslot + lane * bpitch;
+  if (H.snarrow) {  // offsets inside the slice fit 32 bits: one IMAD.WIDE per copy
+    const int sn = int(H.sn), s1 = int(H.s1);
 #pragma unroll 1
-  for (int y = 0; y < H.ny; ++y) {
-    const double* cell = base + int64_t(y) * s1;
+    for (int y = 0; y < H.ny; ++y) {
+      const int oy = y * s1;
 #pragma unroll
-    for (int x = 0; x < L; ++x, cell += sn) cp_async8(bq + L * y + x, cell);
+      for (int x = 0; x < L; ++x) cp_async8(bq + L * y + x, base + (oy + x * sn));
+    }
+  } else {
+    const int64_t sn = H.sn, s1 = H.s1;
+#pragma unroll 1
+    for (int y = 0; y < H.ny; ++y) {
+      const double* cell = base + int64_t(y) * s1;
+#pragma unroll
+      for (int x = 0; x < L; ++x, cell += sn) cp_async8(bq + L * y + x, cell);
+    }
   }
 }
 
@@ -217,10 +227,13 @@ __device__ __forceinline__ void ring_prefetch(const RingHdr& H, const double* __
   const int lane = threadIdx.x & 31;
   const int n = L * H.ny, last = H.cn * 8 - 1;
   const char* const base = reinterpret_cast<const char*>(src + (H.src_off + int64_t(z) * H.s2));
+  const bool nar = H.snarrow != 0;
+  const int sn32 = int(H.sn), s132 = int(H.s1);
 #pragma unroll 1
   for (int c = lane; c < n; c += 32) {
     const int y = c / L, x = c - L * y;
-    const char* const pc = base + 8 * (int64_t(x) * H.sn + int64_t(y) * H.s1);
+    const char* const pc = nar ? base + int64_t(8) * (x * sn32 + y * s132)
+                               : base + 8 * (int64_t(x) * H.sn + int64_t(y) * H.s1);
     l2_prefetch_line(pc);
     l2_prefetch_line(pc + 128);
     l2_prefetch_line(pc + last);
@@ -500,7 +513,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
 #endif
     if (pf && G.tile < n_tiles) ring_prefetch<L>(Hs[G.it & (RG_NH - 1)], src, G.z);
     double chk = 0.0;
-    int k = 0;
+    int k = 0, rd = 0, rd_it = -1;
     while (P.tile < n_tiles) {
 #if !RG_DIRECT
       cp_async_wait_one();  // this thread's copies of slice P landed
@@ -529,11 +542,16 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         ring_phase_a_any<L, D>(H.ny, mybox + (k & 1) * boxd + lane * bpitch, tr0 + s * trd + lane * tpitch, chk);
 #endif
       // blocks that will read this slice: the part's blocks in every row whose window holds it
-      int readers = 0;
-      for (int r = 0; r < H.n2; ++r) {
-        const int w = sgrp[H.g2 + r].x - H.z0;
-        readers += (w <= P.z && P.z < w + L) ? H.n1 : 0;
+      // (lane z of the warp counts them for slice z once per tile)
+      if (P.it != rd_it) {
+        rd_it = P.it;
+        rd = 0;
+        for (int r = 0; r < H.n2; ++r) {
+          const int w = sgrp[H.g2 + r].x - H.z0;
+          rd += (w <= lane && lane < w + L) ? H.n1 : 0;
+        }
       }
+      const int readers = __shfl_sync(0xffffffffu, rd, P.z & 31);
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_expect(&bar_free[s], readers);

@@ -1004,7 +1004,8 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     const int64_t avail = int64_t(fa.maxDynamicSharedSizeBytes) - int64_t(fixed);
     static const int ring_r = [] { const char* e = std::getenv("TH_RING_R"); return e ? std::atoi(e) : RG_RMAX; }();
     const int R = int(std::min<int64_t>(std::min(ring_r, RG_RMAX), avail / (8 * trd)));
-    if (per_sm >= 1 && R >= L + 1) {  // a row's L slices resident plus one being produced
+    // a row's L slices resident plus one being produced; a tile's slices counted by the lanes of a warp
+    if (per_sm >= 1 && R >= L + 1 && op->rg_nzmax <= 32) {
       const size_t smem = fixed + 8 * size_t(trd) * R;
       const int64_t tiles = n_faces * int64_t(op->rg_ntp) * nch;
       const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms())));
