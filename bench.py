@@ -51,7 +51,7 @@ def parse():
                     help="configs 1-4: override the (role:scheme,...) passes, e.g. interpolate:matrix_linear,"
                          "restrict:matrix_linear (extra measurements; the default is BASELINE's)")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--e2e-chunks", type=int, default=16, help="pipeline chunks of the e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=64, help="pipeline chunks of the e2e leg")
     ap.add_argument("--cpu-sample", type=int, default=512, help="faces per pass in the CPU reference arm's sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -784,12 +784,13 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
             batch, ia, ib = chunk_i[c]
             if batch is not None:
                 batch.launch(wl.src, sweep.out["interpolate"], stream=s_run.cuda_stream)
+                run_done()  # interpolation results leave while the chunk's restriction runs
+                d2h(host_i, sweep.out["interpolate"], ia, ib)
             batch, ra, rb = chunk_r[c]
             if batch is not None:
                 batch.launch(wl.src, rout, stream=s_run.cuda_stream)
-            run_done()
-            d2h(host_i, sweep.out["interpolate"], ia, ib)
-            d2h(host_r, rout, ra, rb)
+                run_done()
+                d2h(host_r, rout, ra, rb)
         with torch.cuda.stream(s_run):  # faces that cross ranks (none at N = 1)
             sweep.pre(comp)
             sweep.post(comp)
@@ -832,7 +833,7 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
             "h2d_bytes_per_step": int(n_local * ce * 8),
             "d2h_bytes_per_step": int((rp_i.n_out + nr + sum(r.size for r in rp_r.recv) + rp_r.staged.size) * per * 8),
             "ms_per_step": round(t_step * 1e3, 1), "steps": len(times), "matches_device_run": agree,
-            "how": "per step, 16 chunks of patches: the compact host pool (only the six face slabs of every "
+            "how": f"per step, {n_chunks} chunks of patches: the compact host pool (only the six face slabs of every "
                    "patch that face work reads, 2,160 of 3,375 cells; host memory page-locked with "
                    "cudaHostRegister) -> staging ring (th_memcpy_async) -> device pool (th_pool_blocks); "
                    "interpolation of the faces whose coarse patch arrived, restriction of the faces whose last "
