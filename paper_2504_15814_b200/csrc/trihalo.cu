@@ -1003,7 +1003,10 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     TH_CUDA(cudaFuncGetAttributes(&fa, kfn));
     const int64_t avail = int64_t(fa.maxDynamicSharedSizeBytes) - int64_t(fixed);
     static const int ring_r = [] { const char* e = std::getenv("TH_RING_R"); return e ? std::atoi(e) : RG_RMAX; }();
-    const int R = int(std::min<int64_t>(std::min(ring_r, RG_RMAX), avail / (8 * trd)));
+    // the header ring (RG_NH entries, decoded RG_HAHEAD tiles ahead) must outlast the skew between
+    // the leading A iterator and the slowest warp: (R + (RG_PFD + 1) NA) / L + 2 tiles of >= L slices
+    const int r_hdr = (RG_NH - RG_HAHEAD - 2) * L - (RG_PFD + 1) * NA;
+    const int R = int(std::min<int64_t>(std::min(std::min(ring_r, RG_RMAX), r_hdr), avail / (8 * trd)));
     // a row's L slices resident plus one being produced; a tile's slices counted by the lanes of a warp
     if (per_sm >= 1 && R >= L + 1 && op->rg_nzmax <= 32) {
       const size_t smem = fixed + 8 * size_t(trd) * R;
