@@ -195,11 +195,12 @@ def test_pool_interp_batch(th, scheme, p):
 
 
 @pytest.mark.parametrize("scheme,p,n_face", (("order3", 17, 900), ("order2", 17, 900), ("order3", 9, 1500),
-                                             ("order2", 9, 1500)))
+                                             ("order2", 9, 1500), ("order2", 4, 4000), ("order3", 5, 3000)))
 def test_pool_interp_long_batch(th, scheme, p, n_face):
     """Batches long enough that every persistent CTA walks many tiles (148 CTAs, 2-4 tiles per
     face): the slice ring's slots, their sequence numbers and reader counts are reused tens of
-    times, and the staged tiles run their double buffers in steady state.  Every 7th face plus
+    times, and the staged tiles run their double buffers in steady state (p = 4 / 5: tiles of 3-5
+    slices, the widest skew between the ring's producers and consumers in tiles).  Every 7th face plus
     the last 40 are checked against the oracle; every output value must be written."""
     import torch
 
