@@ -353,9 +353,11 @@ __global__ void __launch_bounds__(NTH, MINB)
   const int64_t t0 = blockIdx.x, step = gridDim.x;
   const bool pf = op.prefetch & 16;  // TH_PREFETCH bit 16: L2 prefetch of the tile after next
   __syncthreads();  // tables filled: the decodes read the group table from shared memory
-  if (threadIdx.x == DEC)
-    for (int i = 0; i < 3; ++i)
-      if (t0 + i * step < n_tiles) tile_decode(op, faces, t0 + i * step, nt, u, Hs[i], sgrp);
+  // the first three headers by three threads of different warps (one latency, not three in a row)
+  if ((threadIdx.x & 31) == 31 && threadIdx.x < 96) {
+    const int i = threadIdx.x >> 5;
+    if (t0 + i * step < n_tiles) tile_decode(op, faces, t0 + i * step, nt, u, Hs[i], sgrp);
+  }
   __syncthreads();
   if (t0 < n_tiles) tile_fetch<NTH>(Hs[0], src, boxes, pitch, u);
   cp_async_commit();
