@@ -145,7 +145,11 @@ __device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double
       double v[5];
 #pragma unroll
       for (int x = 0; x < 5; ++x) v[x] = bz[5 * y + x];
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH >= 3
+      for (int a = 0; a < 4; ++a) mm[y][a] = v[a] + v[4];
+#else
       gram_moments<5, 4>(v, mm[y]);
+#endif
       asm volatile("" ::: "memory");  // one line of loads live at a time (register budget)
     }
     double* const tq = tr + q * T3TP + 10 * z;
@@ -157,7 +161,11 @@ __device__ __forceinline__ void tile3_phase_a_ny(const Tile3Hdr& H, const double
 #pragma unroll
         for (int a = 0; a < 4; ++a) w[y][a] = mm[s + y][a];
       double T[10];
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH >= 3
+      for (int t = 0; t < 10; ++t) T[t] = w[t % 5][t % 4];
+#else
       gram_y<5, 4>(w, T);
+#endif
       // every box value enters some window's T_00 (the windows cover the box's t1 extent)
       chk = fma(T[0], 0.0, chk);
 #pragma unroll
@@ -186,8 +194,13 @@ __device__ __forceinline__ void tile3_item(const double* tq, const T3Syn0& s0, c
       ca[z] = v.x;
       cb[z] = v.y;
     }
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH >= 3
+    for (int k = 0; k < MN[t]; ++k) M[MO[t] + k] = ca[k] + ca[4];
+    for (int k = 0; k < MN[t + 1]; ++k) M[MO[t + 1] + k] = cb[k] + cb[4];
+#else
     gram_moments_n<5>(ca, M + MO[t], MN[t]);
     gram_moments_n<5>(cb, M + MO[t + 1], MN[t + 1]);
+#endif
     asm volatile("" ::: "memory");  // one column pair of loads live at a time
   }
 #pragma unroll
@@ -202,9 +215,14 @@ __device__ __forceinline__ void tile3_item(const double* tq, const T3Syn0& s0, c
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b + a < 4; ++b, ++t) {
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH >= 3
+        Q[t] = M[mi] + S2[b];
+        mi += 4 - a - b;
+#else
         Q[t] = 0.0;
 #pragma unroll
         for (int c = 0; c + b + a < 4; ++c, ++mi) Q[t] = fma(S2[c], M[mi], Q[t]);
+#endif
       }
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -216,16 +234,24 @@ __device__ __forceinline__ void tile3_item(const double* tq, const T3Syn0& s0, c
       int tt = 0;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH >= 2
+        R[a] = Q[a + j] + S1[a];
+#else
         R[a] = 0.0;
 #pragma unroll
         for (int b = 0; b + a < 4; ++b, ++tt) R[a] = fma(S1[b], Q[tt], R[a]);
+#endif
       }
       const OFF oj = qo + OFF(l) * d2 + OFF(j) * d1;
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
+#ifdef TH_AB_NOSYNTH  // diagnosis build: the stores without the last synthesis stage
+        const double oi = R[i];
+#else
         double oi = 0.0;
 #pragma unroll
         for (int a = 0; a < 4; ++a) oi = fma(s0.v[i * 4 + a], R[a], oi);  // constant-bank operands
+#endif
         if (ALL || ok0[i]) *elem(hdst, oj + do0[i]) = oi;
       }
     }
