@@ -252,7 +252,11 @@ __device__ __forceinline__ void tile3_item(const double* tq, const T3Syn0& s0, c
 #pragma unroll
         for (int a = 0; a < 4; ++a) oi = fma(s0.v[i * 4 + a], R[a], oi);  // constant-bank operands
 #endif
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH == 4  // ... and (almost) no stores: one child per block
+        if ((ALL || ok0[i]) && (i + j + l == 0 || oi == 1.2345e300)) *elem(hdst, oj + do0[i]) = oi;
+#else
         if (ALL || ok0[i]) *elem(hdst, oj + do0[i]) = oi;
+#endif
       }
     }
   }
@@ -459,7 +463,11 @@ __device__ __forceinline__ void tile3_fetch_slice(const Tile3Hdr& H, const doubl
   const double* const base = src + (H.src_off + lane + int64_t(z) * H.s2);
   double* const bq = box + lane * T3BOX + 5 * T3Y * z;
 #pragma unroll 1
+#if defined(TH_AB_NOSYNTH) && TH_AB_NOSYNTH == 5  // ... and (almost) no source copies: one line per slice
+  for (int y = 0; y < min(H.ny, 1); ++y) {
+#else
   for (int y = 0; y < H.ny; ++y) {
+#endif
     const double* cell = base + int64_t(y) * s1;
 #pragma unroll
     for (int x = 0; x < 5; ++x, cell += sn) cp_async8(bq + 5 * y + x, cell);
