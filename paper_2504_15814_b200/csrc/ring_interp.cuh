@@ -317,6 +317,133 @@ __device__ __forceinline__ void ring_phase_a_any(int ny, const double* bq, doubl
   else if (ny == L + 3) ring_phase_a<L, D, L + 3>(bq, tq, chk);
 }
 
+// ---- tensor_linear / matrix_linear (ORDER = 1): d-linear 1-D rows in the reference's contraction
+// order, normal -> t1 -> t2 (linear.py:115-151; matrix_linear's collapsed operator is the product
+// of the same rows, linear.py:202-245).  T is per block of the part (the t1 rows differ per block
+// even where the 3-cell windows coincide): T[b1][c0 + 3 c1], 9 values in a slot of 10.
+
+// phase A of one slice: the normal rows of its NY lines, then the t1 rows of every block
+template <int NY>
+__device__ __forceinline__ void ring_phase_a_tensor(const double* bq, double* tq, double& chk, const T3Syn0& r0,
+                                                    const double* stab, const int4* sgrp, int g1, int n1, int y0) {
+  double tx[NY][3];
+#pragma unroll
+  for (int y = 0; y < NY; ++y) {
+    double v[3];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) v[x] = bq[3 * y + x];
+#pragma unroll
+    for (int c0 = 0; c0 < 3; ++c0) {
+      double t = 0.0;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) t = fma(r0.v[c0 * 4 + x], v[x], t);
+      tx[y][c0] = t;
+    }
+    // finiteness of the inputs: every value of the line enters tx[y][0] .. [2] through a
+    // product (0 x Inf and 0 x NaN are NaN), so their sum turns chk NaN for any of them
+    chk = fma((tx[y][0] + tx[y][1]) + tx[y][2], 0.0, chk);
+  }
+#pragma unroll 1
+  for (int b = 0; b < n1; ++b) {
+    const int s = sgrp[g1 + b].x - y0;
+    const double* r1 = stab + (g1 + b) * 12;
+    double R1[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R1[i] = r1[i];
+    double T[10];
+#pragma unroll
+    for (int t = 0; t < 10; ++t) T[t] = 0.0;
+#pragma unroll
+    for (int S = 0; S + 3 <= NY; ++S) {
+      if (s != S) continue;
+#pragma unroll
+      for (int y = 0; y < 3; ++y)
+#pragma unroll
+        for (int c0 = 0; c0 < 3; ++c0)
+#pragma unroll
+          for (int c1 = 0; c1 < 3; ++c1) T[c0 + 3 * c1] = fma(R1[c1 * 3 + y], tx[S + y][c0], T[c0 + 3 * c1]);
+    }
+#pragma unroll
+    for (int t = 0; t < 10; t += 2) *reinterpret_cast<double2*>(tq + b * 10 + t) = make_double2(T[t], T[t + 1]);
+  }
+}
+
+__device__ __forceinline__ void ring_phase_a_tensor_any(int ny, const double* bq, double* tq, double& chk,
+                                                        const T3Syn0& r0, const double* stab, const int4* sgrp, int g1,
+                                                        int n1, int y0) {
+  if (ny == 3) ring_phase_a_tensor<3>(bq, tq, chk, r0, stab, sgrp, g1, n1, y0);
+  else if (ny == 4) ring_phase_a_tensor<4>(bq, tq, chk, r0, stab, sgrp, g1, n1, y0);
+  else if (ny == 5) ring_phase_a_tensor<5>(bq, tq, chk, r0, stab, sgrp, g1, n1, y0);
+  else if (ny == 6) ring_phase_a_tensor<6>(bq, tq, chk, r0, stab, sgrp, g1, n1, y0);
+}
+
+// a block's T values of its 3 slices into registers
+__device__ __forceinline__ void ring_tensor_load(const double* tq, const int (&zo)[3], double (&T)[3][10]) {
+#pragma unroll
+  for (int z = 0; z < 3; ++z)
+#pragma unroll
+    for (int t = 0; t < 10; t += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(tq + zo[z] + t);
+      T[z][t] = v.x;
+      T[z][t + 1] = v.y;
+    }
+}
+
+// the t2 rows of the block at its children, stores
+template <bool ALL, typename OFF>
+__device__ __forceinline__ void ring_tensor_out(const double (&T)[3][10], const double* r2, double* __restrict__ hdst,
+                                                OFF qo, OFF d1, OFF d2, const OFF (&do0)[3], const bool (&ok0)[3],
+                                                const bool (&ok1)[3], const bool (&ok2)[3]) {
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    if (!ALL && !ok2[l]) continue;
+    double o[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) o[t] = 0.0;
+#pragma unroll
+    for (int z = 0; z < 3; ++z) {
+      const double w = r2[l * 3 + z];
+#pragma unroll
+      for (int t = 0; t < 9; ++t) o[t] = fma(w, T[z][t], o[t]);
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (!ALL && !ok1[j]) continue;
+      const OFF oj = qo + OFF(l) * d2 + OFF(j) * d1;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (ALL || ok0[i]) *elem(hdst, oj + do0[i]) = o[i + 3 * j];
+    }
+  }
+}
+
+template <typename OFF>
+__device__ __forceinline__ void ring_tensor_block(const RingHdr& H, const DevOp& op, double* __restrict__ dst,
+                                                  const double (&T)[3][10], const double* stab, int4 G1, int4 G2,
+                                                  int g2) {
+  const int4 G0 = H.G0;
+  bool ok0[3], ok1[3], ok2[3];
+  OFF do0[3];
+  bool all = true;
+  const int p = op.p;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int t = G0.z + i;
+    ok0[i] = i < G0.w && t >= 0 && t < op.k;
+    do0[i] = OFF(t) * OFF(H.dn);
+    ok1[i] = i < G1.w && unsigned(G1.z + i - H.lo1) < unsigned(p);
+    ok2[i] = i < G2.w && unsigned(G2.z + i - H.lo2) < unsigned(p);
+    all &= ok0[i] & ok1[i] & ok2[i];
+  }
+  const OFF d1 = OFF(H.d1), d2 = OFF(H.d2);
+  const int q = threadIdx.x & 31;
+  const OFF qo = OFF(G1.z - H.lo1) * d1 + OFF(G2.z - H.lo2) * d2 + OFF(H.cb + q);
+  double* const hdst = dst + H.dst_off;
+  const double* r2 = stab + g2 * 12;
+  if (all) ring_tensor_out<true, OFF>(T, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+  else ring_tensor_out<false, OFF>(T, r2, hdst, qo, opaque(d1), opaque(d2), do0, ok0, ok1, ok2);
+}
+
 // t2 moments of a block: the pairs (a, b) of its window start, L ring slices at zo[]
 // (moment index: a-major, then b, then c; D - a - b moments per pair)
 template <int L, int D>
@@ -428,7 +555,10 @@ __global__ void __launch_bounds__(RG_NTH, 1)
     ring_interp_kernel(DevOp op, T3Syn0 syn0, const double* __restrict__ src, double* __restrict__ dst,
                        const th_face* __restrict__ faces, int64_t n_tiles, int ntp, int nch, int cmax, int u, int NA,
                        int R, int bpitch, int tpitch, int32_t* flag) {
-  constexpr int L = ORDER == 2 ? 3 : 5, D = ORDER + 1, NP = D * (D + 1) / 2, NM = ORDER == 2 ? 10 : 20;
+  // ORDER 1: tensor_linear / matrix_linear (3-cell windows, T per block); 2 / 3: Gram least squares
+  constexpr bool TENSOR = ORDER == 1;
+  constexpr int L = ORDER == 3 ? 5 : 3, D = TENSOR ? 3 : ORDER + 1, NP = TENSOR ? 10 : D * (D + 1) / 2;
+  constexpr int NM = ORDER == 3 ? 20 : 10;
   extern __shared__ __align__(16) double smem_rg[];
   __shared__ RingHdr Hs[RG_NH];
   __shared__ __align__(8) uint64_t bar_free[RG_RMAX], bar_hdr[RG_NH];
@@ -442,7 +572,14 @@ __global__ void __launch_bounds__(RG_NTH, 1)
   double* const tr0 = box0 + (RG_DIRECT ? 0 : NA * 2 * boxd);
   const int NB = RG_NW - NA;
   for (int i = threadIdx.x; i < G1n; i += RG_NTH) sgrp[i] = __ldg(&op.grp1[i]);
-  for (int i = threadIdx.x; i < G1n * 12; i += RG_NTH) stab[i] = __ldg(op.synth1 + i);
+  if constexpr (TENSOR) {  // t1 / t2 rows [group][child][3] in slots of 12, absent children zero
+    for (int i = threadIdx.x; i < G1n * 12; i += RG_NTH) {
+      const int g = i / 12, r = i - g * 12, c = r / 3;
+      stab[i] = (r < 9 && c < __ldg(&op.grp1[g]).w) ? __ldg(op.rows1 + __ldg(&op.row_off1[g]) + r) : 0.0;
+    }
+  } else {
+    for (int i = threadIdx.x; i < G1n * 12; i += RG_NTH) stab[i] = __ldg(op.synth1 + i);
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < RG_RMAX; ++i) ready[i] = 0;
     for (int i = 0; i < RG_RMAX; ++i) mbar_init(&bar_free[i], 1);
@@ -531,6 +668,7 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         rg_wait_relaxed(&bar_free[s], (gz / R - 1) & 1);
       }
 #if RG_DIRECT
+      static_assert(!TENSOR, "RG_DIRECT: Gram schemes only");
       if (lane < H.cn) {
         const double* const base = src + (H.src_off + lane + int64_t(P.z) * H.s2);
         double* const tq = tr0 + s * trd + lane * tpitch;
@@ -538,8 +676,12 @@ __global__ void __launch_bounds__(RG_NTH, 1)
         else ring_phase_a_direct_any<L, D, int64_t>(H.ny, base, H.sn, H.s1, tq, chk);
       }
 #else
-      if (lane < H.cn)
-        ring_phase_a_any<L, D>(H.ny, mybox + (k & 1) * boxd + lane * bpitch, tr0 + s * trd + lane * tpitch, chk);
+      if (lane < H.cn) {
+        const double* const bq = mybox + (k & 1) * boxd + lane * bpitch;
+        double* const tq = tr0 + s * trd + lane * tpitch;
+        if constexpr (TENSOR) ring_phase_a_tensor_any(H.ny, bq, tq, chk, syn0, stab, sgrp, H.g1, H.n1, H.y0);
+        else ring_phase_a_any<L, D>(H.ny, bq, tq, chk);
+      }
 #endif
       // blocks that will read this slice: the part's blocks in every row whose window holds it
       // (lane z of the warp counts them for slice z once per tile)
@@ -613,16 +755,30 @@ __global__ void __launch_bounds__(RG_NTH, 1)
           for (int j = 0; j < L; ++j) ok &= lds_acquire(&ready[sl[j]]) == gzb + dz + j + 1;
           if (ok) break;
         }
-        double M[NM];
-        if (active) ring_moments<L, D>(tr0 + lane * tpitch + (G1.x - y0) * NP, zo, M);
-        __syncwarp();
-        if (lane == 0) {  // this block has read its slices
+        if constexpr (TENSOR) {
+          double T[3][10];
+          if (active) ring_tensor_load(tr0 + lane * tpitch + b1 * NP, zo, T);
+          __syncwarp();
+          if (lane == 0) {  // this block has read its slices
 #pragma unroll
-          for (int j = 0; j < L; ++j) mbar_complete_tx(&bar_free[sl[j]], 1);
-        }
-        if (active) {
-          if (H.narrow) ring_block<D, int>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
-          else ring_block<D, int64_t>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
+            for (int j = 0; j < L; ++j) mbar_complete_tx(&bar_free[sl[j]], 1);
+          }
+          if (active) {
+            if (H.narrow) ring_tensor_block<int>(H, op, dst, T, stab, G1, G2, g2);
+            else ring_tensor_block<int64_t>(H, op, dst, T, stab, G1, G2, g2);
+          }
+        } else {
+          double M[NM];
+          if (active) ring_moments<L, D>(tr0 + lane * tpitch + (G1.x - y0) * NP, zo, M);
+          __syncwarp();
+          if (lane == 0) {  // this block has read its slices
+#pragma unroll
+            for (int j = 0; j < L; ++j) mbar_complete_tx(&bar_free[sl[j]], 1);
+          }
+          if (active) {
+            if (H.narrow) ring_block<D, int>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
+            else ring_block<D, int64_t>(H, op, dst, M, stab, syn0, G1, G2, g1, g2);
+          }
         }
       }
       slotb += H.nz;

@@ -417,6 +417,7 @@ struct th_operator {
   // slice-ring interpolation (ring_interp.cuh): window length (0 = not eligible), t1 parts per
   // face, and the largest line / window-start / slice counts of a tile
   int rg_L = 0, rg_ntp = 1, rg_nymax = 0, rg_nsmax = 0, rg_nzmax = 0;
+  bool rg_tensor = false;  // d-linear 1-D rows (tensor_linear, matrix_linear in factored form) instead of Gram moments
 };
 
 namespace {
@@ -612,11 +613,17 @@ void prepare_tile3(th_operator* op) {
 void prepare_ring(th_operator* op) {
   const th::HostOperator& h = op->host;
   op->rg_L = 0;
-  if (h.role != 0 || (h.scheme != TH_SCHEME_ORDER2 && h.scheme != TH_SCHEME_ORDER3) || !h.gram_ok ||
-      h.fast_C0 != 3 || h.synth[0].size() < 12 || h.synth[1].empty() || h.groups[0].size() != 1 ||
-      h.groups[1].empty())
-    return;
-  const int L = h.scheme == TH_SCHEME_ORDER2 ? 3 : 5;
+  op->rg_tensor = false;
+  if (h.role != 0 || h.groups[0].size() != 1 || h.groups[1].empty()) return;
+  // tensor_linear, and matrix_linear in factored form (the collapsed operator is the product of
+  // the same 1-D rows, linear.py:202-245; cf. prepare_tile)
+  const bool linear_rows = (h.fast_mode == 2 || (h.fast_mode == 1 && h.scheme == TH_SCHEME_MATRIX_LINEAR)) &&
+                           h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3 && !h.rows[0].empty() &&
+                           !h.rows[1].empty();
+  const bool gram = (h.scheme == TH_SCHEME_ORDER2 || h.scheme == TH_SCHEME_ORDER3) && h.gram_ok && h.fast_C0 == 3 &&
+                    h.synth[0].size() >= 12 && !h.synth[1].empty();
+  if (!linear_rows && !gram) return;
+  const int L = linear_rows ? 3 : h.scheme == TH_SCHEME_ORDER2 ? 3 : 5;
   const th::Group& g0 = h.groups[0][0];
   if (g0.winL != L || g0.tgtN < 1 || g0.tgtN > 3) return;
   const auto& g1 = h.groups[1];
@@ -640,11 +647,12 @@ void prepare_ring(th_operator* op) {
         const int ny = g1[b - 1].win0 + L - g1[a].win0;
         ok = b - a <= RG_NS && ny <= L + 3;
         nymax = std::max(nymax, ny);
-        nsmax = std::max(nsmax, ny - L + 1);
+        nsmax = std::max(nsmax, linear_rows ? b - a : ny - L + 1);  // T entries per slice: blocks / window starts
       }
     }
     if (ok) {
       op->rg_L = L;
+      op->rg_tensor = linear_rows;
       op->rg_ntp = ntp;
       op->rg_nymax = nymax;
       op->rg_nsmax = nsmax;
@@ -976,26 +984,30 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   const bool gram = h.gram_ok && h.fast_C0 == 3;
   const bool tensor_fast = h.fast_mode == 2 && h.fast_L0 == 3 && h.fast_C0 == 3 && h.fast_CT == 3;
   static const int use_tile = [] { const char* e = std::getenv("TH_TILE"); return e ? std::atoi(e) : 1; }();
-  //   TH_RING bits (default 3)   1: order3 interpolation through the slice ring (ring_interp.cuh)
+  //   TH_RING bits (default 11)  1: order3 interpolation through the slice ring (ring_interp.cuh)
   //                                 where the order3 tiles do not fit (p = 17)
   //                              2: order2 interpolation likewise, where the 3-cell tiles do not fit
+  //                              8: tensor_linear / matrix_linear interpolation likewise
   //                              4: the slice ring instead of the tile kernels wherever it fits
-  //   TH_RING_NA, TH_RING_R      A warps / ring slots of the slice ring (defaults: 7 A warps for
-  //                              rows of <= 3 blocks, 5 otherwise; as many slots as fit)
-  static const int use_ring = [] { const char* e = std::getenv("TH_RING"); return e ? std::atoi(e) : 3; }();
+  //   TH_RING_NA, TH_RING_R      A warps / ring slots of the slice ring (defaults: Gram 7 A warps for
+  //                              rows of <= 3 blocks, 5 otherwise, d-linear 8; as many slots as fit)
+  static const int use_ring = [] { const char* e = std::getenv("TH_RING"); return e ? std::atoi(e) : 11; }();
   static const int ring_na = [] { const char* e = std::getenv("TH_RING_NA"); return e ? std::atoi(e) : 0; }();
   auto ring_launch = [&]() -> int32_t {
-    const int L = op->rg_L, NP = L == 5 ? 10 : 6;
+    const int L = op->rg_L, NP = (L == 5 || op->rg_tensor) ? 10 : 6;
     const int nch = (u + 31) / 32;
     int cmax = 0;
     for (int c = 0; c < nch; ++c) cmax = std::max(cmax, int(int64_t(c + 1) * u / nch - int64_t(c) * u / nch));
-    const int NA = std::min(std::max(ring_na > 0 ? ring_na : (op->rg_nsmax <= 3 ? 7 : 5), 1), RG_NW - RG_NS);
+    // (measured defaults, profiles/r02_ab_ring.txt: the d-linear rows leave the B warps little to do)
+    const int na_default = op->rg_tensor ? 8 : op->rg_nsmax <= 3 ? 7 : 5;
+    const int NA = std::min(std::max(ring_na > 0 ? ring_na : na_default, 1), RG_NW - RG_NS);
     const int bpitch = (L * op->rg_nymax) | 1;
     int tpitch = op->rg_nsmax * NP;
     while (tpitch % 4 != 2) ++tpitch;  // 16-byte accesses of consecutive lanes conflict-free
     const int64_t boxd = (int64_t(cmax) * bpitch + 1) & ~int64_t(1), trd = int64_t(cmax) * tpitch;
-    const void* kfn = L == 5 ? reinterpret_cast<const void*>(ring_interp_kernel<3>)
-                             : reinterpret_cast<const void*>(ring_interp_kernel<2>);
+    const void* kfn = op->rg_tensor ? reinterpret_cast<const void*>(ring_interp_kernel<1>)
+                      : L == 5      ? reinterpret_cast<const void*>(ring_interp_kernel<3>)
+                                    : reinterpret_cast<const void*>(ring_interp_kernel<2>);
     int per_sm = 0;
     const size_t fixed = 8 * (size_t(ring_fixed_doubles(op->dev.G1)) + (RG_DIRECT ? 0 : size_t(NA) * 2 * boxd));
     TH_CUDA(resident_ctas(kfn, RG_NTH, fixed + 8 * size_t(trd) * (L + 1), &per_sm));
@@ -1013,8 +1025,18 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
       const int64_t tiles = n_faces * int64_t(op->rg_ntp) * nch;
       const int tblocks = int(std::min<int64_t>(tiles, int64_t(num_sms())));
       T3Syn0 syn0;
-      std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
-      if (L == 5)
+      if (op->rg_tensor) {  // the normal rows [child][3] in slots of 4, absent children zero
+        std::fill(syn0.v, syn0.v + 12, 0.0);
+        const th::Group& g0 = h.groups[0][0];
+        for (int c = 0; c < g0.tgtN && c < 3; ++c)
+          for (int x = 0; x < 3; ++x) syn0.v[c * 4 + x] = h.rows[0][size_t(h.row_off[0][0]) + c * 3 + x];
+      } else {
+        std::copy(h.synth[0].begin(), h.synth[0].begin() + 12, syn0.v);
+      }
+      if (op->rg_tensor)
+        ring_interp_kernel<1><<<tblocks, RG_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, op->rg_ntp, nch,
+                                                            cmax, u, NA, R, bpitch, tpitch, flag);
+      else if (L == 5)
         ring_interp_kernel<3><<<tblocks, RG_NTH, smem, s>>>(op->dev, syn0, src, dst, faces, tiles, op->rg_ntp, nch,
                                                             cmax, u, NA, R, bpitch, tpitch, flag);
       else
@@ -1025,7 +1047,7 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
     }
     return -1;  // does not fit: the caller falls through to the next kernel
   };
-  const bool ring_ok = interp && op->rg_L && (use_ring & (op->rg_L == 5 ? 1 : 2));
+  const bool ring_ok = interp && op->rg_L && (use_ring & (op->rg_tensor ? 8 : op->rg_L == 5 ? 1 : 2));
   if (ring_ok && (use_ring & 4)) {
     const int32_t rc = ring_launch();
     if (rc >= 0) return rc;

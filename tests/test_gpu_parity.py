@@ -195,7 +195,9 @@ def test_pool_interp_batch(th, scheme, p):
 
 
 @pytest.mark.parametrize("scheme,p,n_face", (("order3", 17, 900), ("order2", 17, 900), ("order3", 9, 1500),
-                                             ("order2", 9, 1500), ("order2", 4, 4000), ("order3", 5, 3000)))
+                                             ("order2", 9, 1500), ("order2", 4, 4000), ("order3", 5, 3000),
+                                             ("tensor_linear", 17, 900), ("matrix_linear", 17, 900),
+                                             ("tensor_linear", 9, 1500), ("matrix_linear", 5, 3000)))
 def test_pool_interp_long_batch(th, scheme, p, n_face):
     """Batches long enough that every persistent CTA walks many tiles (148 CTAs, 2-4 tiles per
     face): the slice ring's slots, their sequence numbers and reader counts are reused tens of
@@ -390,15 +392,15 @@ def test_pool_transposed_layout(th, scheme, p):
 
 
 @pytest.mark.parametrize("env", ({"TH_GRAM": "3"}, {"TH_TILE": "0"}, {"TH_TILE3": "0"},
-                                 {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_RING": "7"},
-                                 {"TH_RING": "7", "TH_RING_NA": "3", "TH_RING_R": "6"}, {"TH_RING": "0"}))
+                                 {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_RING": "15"},
+                                 {"TH_RING": "15", "TH_RING_NA": "3", "TH_RING_R": "6"}, {"TH_RING": "0"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
     parity tests in a child process with the alternative paths (the per-warp order3
     restriction slide; the per-warp interpolation slide instead of the staged tile kernel;
     the per-warp slide for order3 interpolation instead of the two-phase order3 tiles; the
     fixed-window kernels with neither tiles nor Gram slides; the slice ring (ring_interp.cuh)
-    for every order2 / order3 interpolation, also with 3 A warps and the smallest ring; the
+    for every interpolation (Gram and d-linear), also with 3 A warps and the smallest ring; the
     per-warp slide instead of the slice ring at p = 17)."""
     import os
     import subprocess
