@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of the slice-ring interpolation kernel (TH_RING) against the defaults:
-#   gpurun -- 'bash tools/ab_ring.sh parity|bench [NA ...]'
+#   gpurun -- 'bash tools/ab_ring.sh parity|bench [NA ...]'   (TH_RING=15: the ring for every interpolation)
 mkdir -p gpurun_out
 mode=$1; shift
 sel="exchange_all_faces_small or pool_interp_batch or pool_interp_long_batch or pool_restrict_batch or transposed or unknown_counts"
