@@ -350,8 +350,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 #else
         if (active) {
 #endif
-          const int* h = hdr + s * 4;
-          const int XS = h[0], YS = h[1], BASE = h[2];
+          const int4 h = *reinterpret_cast<const int4*>(hdr + s * 4);  // (16-byte aligned: one load)
+          const int XS = h.x, YS = h.y, BASE = h.z;
           const double* st = stages + size_t(s) * stage_d + BASE + cb + lane;
           const unsigned* el = eline + s * ny_max + ly;
           // a window the slice does not reach reads the zero block; lanes past u read whatever
@@ -363,11 +363,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
           for (int y = 0; y < L; ++y) {
             const unsigned e = el[y];
             const double* ln = st + (ly + y) * YS;
+            // the line's 4 + 4 folded weights through four 16-byte broadcast loads (the tables sit on
+            // 32-byte boundaries: stage_d is even and every table offset a multiple of 4 doubles)
             double WA[D], WB[D];
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-              WA[i] = wa[y * 4 + i];
-              WB[i] = wb[y * 4 + i];
+            static_assert(D == 4, "order3: four degrees");
+            {
+              const double2 a0 = *reinterpret_cast<const double2*>(wa + y * 4),
+                            a1 = *reinterpret_cast<const double2*>(wa + y * 4 + 2),
+                            b0 = *reinterpret_cast<const double2*>(wb + y * 4),
+                            b1 = *reinterpret_cast<const double2*>(wb + y * 4 + 2);
+              WA[0] = a0.x, WA[1] = a0.y, WA[2] = a1.x, WA[3] = a1.y;
+              WB[0] = b0.x, WB[1] = b0.y, WB[2] = b1.x, WB[3] = b1.y;
             }
 #pragma unroll
             for (int q = 0; q < NU; ++q) {
