@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=512, help="faces per pass in the CPU reference arm's sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true", help="skip the sustained-copy yardstick (config 5)")
     ap.add_argument("--no-same-level", action="store_true", help="skip the same-level halo fill leg")
     ap.add_argument("--overlap", action="store_true", help="A/B: interpolation passes on a side stream (diagnosis)")
     ap.add_argument("--reverse-passes", action="store_true", help="run the step's passes in reverse order (diagnosis)")
@@ -131,6 +132,47 @@ class ClockSampler:
         reasons = sorted({names[i] for r in inside for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(float(r[0]) for r in inside), "sm_max_mhz": float(inside[0][1]),
                 "reasons": reasons, "samples": len(inside)}
+
+
+def sustained_copy(dev, index: int, seconds: float = 2.0):
+    """The copy yardstick of MEASURED_PEAKS.json (b.copy_(a) over 1 Gi bf16 elements, read + write
+    bytes) run back to back for `seconds` on this box, right after the timed sweeps: what a plain
+    copy sustains under the same power cap the sweep runs into (the peak itself is a best-of-10
+    burst).  Reported beside the roofline, never used as its denominator."""
+    import torch
+
+    try:
+        a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+        b = torch.empty_like(a)
+    except RuntimeError as exc:  # out of memory beside a large workload
+        return {"error": str(exc).splitlines()[0]}
+    a.zero_()
+    nbytes = 2 * a.numel() * a.element_size()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(10):
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    n = max(30, int(seconds * best * 1e9 / nbytes))
+    sampler = ClockSampler(index)
+    sampler.start()
+    for _ in range(n // 3):  # a third of the run to reach the sustained state
+        b.copy_(a)
+    torch.cuda.synchronize()
+    sampler.mark()
+    e0.record()
+    for _ in range(n - n // 3):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    gbs = (n - n // 3) * nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del a, b
+    return {"GBps": round(gbs, 1), "burst_GBps": round(best, 1), "seconds": round(e0.elapsed_time(e1) / 1e3, 2),
+            "clocks": clocks, "how": "b.copy_(a), 1 Gi bf16 elements, back to back; read + write bytes"}
 
 
 # ---------------------------------------------------------------------------
@@ -625,6 +667,11 @@ def run_multi(args, rank, world, local_rank):
                                                  f"of one ncu --set full launch over {ent['faces']} faces, per face)")
     except (OSError, ValueError):
         pass
+    if not args.no_sustained:
+        sc = sustained_copy(dev, local_rank)
+        res["roofline"]["sustained_copy"] = sc
+        if "GBps" in sc:
+            res["roofline"]["frac_sustained_copy"] = round(rows[dom]["alg_GBps"] / sc["GBps"], 4)
     if not args.no_e2e:
         res["e2e"] = run_c5_e2e(args, wl, plan, sweep, comp, ops, p, k, u, lo, dev, world)
     res["parity"] = c5_parity(wl, plan, sweep, per, world)
