@@ -809,8 +809,19 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
         e.record(s_run)
         s_out.wait_event(e)
 
+    trace = [] if os.environ.get("TH_E2E_TRACE") else None  # diagnosis: per-chunk stream timeline
+
+    def tr(stream, what, c):
+        if trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            trace.append((what, c, e))
+
     def e2e_step():
         unpacked = [None] * n_chunks
+        if trace is not None:
+            trace.clear()
+            tr(s_in, "t0", -1)
         for c in range(n_chunks):
             a, b = cb[c], cb[c + 1]
             st = staging[c % 3]
@@ -819,6 +830,7 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
             if b > a:
                 _native.check(lib.th_memcpy_async(st.data_ptr(), host_compact.ctypes.data + a * ce * 8,
                                                   (b - a) * ce * 8, 0, s_in.cuda_stream))
+            tr(s_in, "h2d", c)
             ev = torch.cuda.Event()
             ev.record(s_in)
             s_run.wait_event(ev)
@@ -833,11 +845,14 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
                 batch.launch(wl.src, sweep.out["interpolate"], stream=s_run.cuda_stream)
                 run_done()  # interpolation results leave while the chunk's restriction runs
                 d2h(host_i, sweep.out["interpolate"], ia, ib)
+                tr(s_out, "d2h_i", c)
             batch, ra, rb = chunk_r[c]
             if batch is not None:
                 batch.launch(wl.src, rout, stream=s_run.cuda_stream)
+                tr(s_run, "run", c)
                 run_done()
                 d2h(host_r, rout, ra, rb)
+                tr(s_out, "d2h_r", c)
         with torch.cuda.stream(s_run):  # faces that cross ranks (none at N = 1)
             sweep.pre(comp)
             sweep.post(comp)
@@ -858,6 +873,11 @@ def _c5_e2e_run(args, wl, plan, sweep, comp, p, k, u, dev, world, st):
         e2e_step()
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t)
+    if trace:
+        t0e = trace[0][2]
+        for what, c, e in trace[1:]:
+            if c % 8 == 7 or c == n_chunks - 1:
+                print(f"e2e trace chunk {c:3d} {what:6s} {t0e.elapsed_time(e):8.1f} ms", file=sys.stderr)
     t_step = statistics.median(times)
     if world > 1:
         tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
