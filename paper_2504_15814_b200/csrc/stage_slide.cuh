@@ -69,7 +69,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 }  // namespace stage
 
-template <int ROLE, int ORDER, bool TENSOR, int NCW, int NST, int NU, int MINB>
+template <int ROLE, int ORDER, bool TENSOR, int NCW, int NST, int NU, int MINB, bool OWN = false>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     stage_slide_kernel(DevOp op, const double* __restrict__ src, double* __restrict__ dst,
                        const th_face* __restrict__ faces, int64_t n_faces, int u, int32_t* flag, int stage_d,
@@ -83,10 +83,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   double* const wtab = sm + NST * stage_d;                  // ROLE 1: [class pair][z][y][a] folded weights
   // ROLE 1: 20 zeros after the table, the weights of a t2 window a slice does not reach
   double* const wzero = wtab + op.st_ncls * op.st_ncls * 100;
-  int* const hdr = reinterpret_cast<int*>(wzero + 20);                              // [NST][4]
+  // OWN: hand-over slots of the line-owner consumers, [NCW - 1][NU][D][32] (see below)
+  constexpr int XSLOT = NU * (ORDER + 1) * 32;
+  double* const xch = wzero + 20;
+  int* const hdr = reinterpret_cast<int*>(xch + (OWN ? (NCW - 1) * XSLOT : 0));     // [NST][4]
   unsigned* const eline = reinterpret_cast<unsigned*>(hdr + NST * 4);             // [NST][ny_max]
   unsigned char* const shr = reinterpret_cast<unsigned char*>(eline + NST * ny_max);  // producer scratch
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ __align__(8) uint64_t xfull[OWN ? NCW : 1], xempty[OWN ? NCW : 1];
   // group table and synthesis-row classes in shared memory: a tile's header (face record ->
   // groups -> classes) then costs one global-memory latency instead of a chain of four, which
   // every consumer warp used to wait out at the start of each tile while the ring stood full
@@ -107,6 +111,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       mbar_init(&full[s], 32);
       mbar_init(&empty[s], NCW);
     }
+    if constexpr (OWN)
+      for (int i = 0; i < NCW; ++i) {
+        mbar_init(&xfull[i], 1);
+        mbar_init(&xempty[i], 1);
+      }
     mbar_fence_init();
   }
   if constexpr (ROLE == 1) {
@@ -307,7 +316,189 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     }
   } else {
     // ===================== consumers =====================
-    if constexpr (ROLE == 1) {
+    if constexpr (ROLE == 1 && OWN) {
+    // LINE-OWNER consumers (u <= 64, tiles of <= NCW - 1 groups).  t1 windows step by 3 and are 5
+    // lines long, so with one warp per t1 group every warp projects 5 lines per slice and 2 of
+    // every 3 lines are projected twice.  Here every line of the slice has ONE owner: warp i < ng
+    // owns the lines [w_i, w_{i+1}) -- the lines group i shares with group i - 1 plus its own --
+    // (the last group: its first 3 lines; warp ng, the helper, its last 2): <= 3 lines per warp
+    // and slice.  A line's normal moments feed the owner's OWN group (window i) and, where the
+    // line also lies in window i - 1, the partial sums it keeps for the PREVIOUS group.  When a
+    // t2 window completes, warp i hands its partial of group i - 1 to warp i - 1 through a
+    // shared-memory slot (full / empty mbarriers per slot, one writer and one reader warp each;
+    // partials are written before the own group's are awaited, so the chain resolves from the
+    // helper down) and warp i - 1 adds it to its own before the normal synthesis.
+    int s = 0;
+    unsigned ph = 0, xin = 0, xout = 0;
+    const int ncl = op.st_ncls;
+    const int i = warp;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int64_t f = tile / tiles_per_face;
+      const th_face* fp = faces + f;
+      FaceRef fr;
+      decode_face_restrict(fp, op, fr);
+      Tile t;
+      if (!tile_of(grp, fr, int(tile - f * tiles_per_face), tg, L, t)) continue;
+      const int ng = t.gB - t.gA;
+      const bool active = i <= ng, hasOwn = i < ng, hasPrev = active && i >= 1;
+      const int gO = t.gA + (hasOwn ? i : ng - 1), gP = t.gA + (hasPrev ? i - 1 : 0);
+      const int wO = grp[gO].x, wP = grp[gP].x, wl = grp[t.gB - 1].x;
+      const int la = i < ng ? wO : wl + 3;
+      const int lb = i < ng - 1 ? grp[gO + 1].x : i == ng - 1 ? wl + 3 : wl + L;
+      const int nl = active ? lb - la : 0;  // <= 3 (stage_geometry)
+      const int ly = la - t.y0;
+      bool ownS[3], prevS[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        ownS[k] = hasOwn && la + k < wO + L;
+        prevS[k] = hasPrev && la + k < wP + L;
+      }
+      const int yo = (la - wO) * 4, yp = (la - wP) * 4;  // first line's row in the own / previous window
+      const double* const wrowO = wtab + cls[gO] * ncl * 100;
+      const double* const wrowP = wtab + cls[gP] * ncl * 100;
+      bool ok[NU];
+#pragma unroll
+      for (int q = 0; q < NU; ++q) ok[q] = hasOwn && lane + 32 * q < u;
+      double UA[NU][D], UB[NU][D], PA[NU][D], PB[NU][D];
+#pragma unroll
+      for (int q = 0; q < NU; ++q)
+#pragma unroll
+        for (int a = 0; a < D; ++a) UA[q][a] = UB[q][a] = PA[q][a] = PB[q][a] = 0.0;
+      int j = 0;
+      int wA = grp[0].x;
+      int wB = G1 > 1 ? grp[1].x : INT_MAX / 2;
+      int cA = cls[0], cB = G1 > 1 ? cls[1] : 0;
+      bool bad = false;
+      for (int a2 = t.z0; a2 < t.z1; ++a2) {
+        const int zA = a2 - wA, zB = a2 - wB;
+        const bool inA = zA >= 0 && zA < L, inB = zB >= 0 && zB < L;
+        mbar_wait(&full[s], ph);
+        if (nl > 0) {
+          const int4 h = *reinterpret_cast<const int4*>(hdr + s * 4);
+          const int XS = h.x, YS = h.y, BASE = h.z;
+          const double* st = stages + size_t(s) * stage_d + BASE + lane;
+          const unsigned* el = eline + s * ny_max + ly;
+          const int oA = cA * 100 + zA * 20, oB = cB * 100 + zB * 20;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (k >= nl) break;
+            const unsigned e = el[k];
+            const double* ln = st + (ly + k) * YS;
+            double m[NU][D];
+#pragma unroll
+            for (int q = 0; q < NU; ++q) {
+              double v[L];
+#pragma unroll
+              for (int x = 0; x < L; ++x) v[x] = ln[x * XS + int((e >> (6 * x)) & 63u) + 32 * q];
+              gram_moments<L, D>(v, m[q]);
+            }
+            static_assert(D == 4, "order3: four degrees");
+            if (ownS[k]) {
+              const double* wa = inA ? wrowO + oA + yo + k * 4 : wzero;
+              const double* wb = inB ? wrowO + oB + yo + k * 4 : wzero;
+              const double2 a0 = *reinterpret_cast<const double2*>(wa), a1 = *reinterpret_cast<const double2*>(wa + 2),
+                            b0 = *reinterpret_cast<const double2*>(wb), b1 = *reinterpret_cast<const double2*>(wb + 2);
+              const double WA[D] = {a0.x, a0.y, a1.x, a1.y}, WB[D] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+              for (int q = 0; q < NU; ++q)
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                  UA[q][a] = fma(WA[a], m[q][a], UA[q][a]);
+                  UB[q][a] = fma(WB[a], m[q][a], UB[q][a]);
+                }
+            }
+            if (prevS[k]) {
+              const double* wa = inA ? wrowP + oA + yp + k * 4 : wzero;
+              const double* wb = inB ? wrowP + oB + yp + k * 4 : wzero;
+              const double2 a0 = *reinterpret_cast<const double2*>(wa), a1 = *reinterpret_cast<const double2*>(wa + 2),
+                            b0 = *reinterpret_cast<const double2*>(wb), b1 = *reinterpret_cast<const double2*>(wb + 2);
+              const double WA[D] = {a0.x, a0.y, a1.x, a1.y}, WB[D] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+              for (int q = 0; q < NU; ++q)
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                  PA[q][a] = fma(WA[a], m[q][a], PA[q][a]);
+                  PB[q][a] = fma(WB[a], m[q][a], PB[q][a]);
+                }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (!active) continue;
+        if (zA == L - 1) {
+          // ---- window j complete ----
+          if (hasPrev) {  // the partial of group i - 1 to its warp
+            double* xs = xch + (i - 1) * XSLOT + lane;
+            mbar_wait(&xempty[i - 1], xout ^ 1);
+#pragma unroll
+            for (int q = 0; q < NU; ++q)
+#pragma unroll
+              for (int a = 0; a < D; ++a) xs[(q * D + a) * 32] = PA[q][a];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xfull[i - 1]);
+            xout ^= 1;
+          }
+          if (hasOwn) {
+            const double* xs = xch + i * XSLOT + lane;
+            mbar_wait(&xfull[i], xin);
+#pragma unroll
+            for (int q = 0; q < NU; ++q)
+#pragma unroll
+              for (int a = 0; a < D; ++a) UA[q][a] += xs[(q * D + a) * 32];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xempty[i]);
+            xin ^= 1;
+            // its normal children, store
+            const int t1 = grp[gO].z, t2 = grp[j].z;
+            if (t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p) {
+              const int4 G0 = fr.g0 == 0 ? G0c : __ldg(&op.grp0[fr.g0]);
+              const double* s0 = op.synth0 + fr.g0 * 12;
+              double* const ob = dst + fr.dst + int64_t(t1 - fr.lo1) * fr.d1 + int64_t(t2 - fr.lo2) * fr.d2 + lane;
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                const int t0 = G0.z + c;
+                if (c < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) {
+                  double S0[D];
+#pragma unroll
+                  for (int a = 0; a < D; ++a) S0[a] = __ldg(s0 + c * 4 + a);
+#pragma unroll
+                  for (int q = 0; q < NU; ++q) {
+                    double o = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) o = fma(S0[a], UA[q][a], o);
+                    if (ok[q]) {
+                      ob[int64_t(t0 - fr.lo0) * fr.dn + 32 * q] = o;
+                      bad |= !isfinite(o);
+                    }
+                  }
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < NU; ++q)
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              UA[q][a] = UB[q][a];
+              UB[q][a] = 0.0;
+              PA[q][a] = PB[q][a];
+              PB[q][a] = 0.0;
+            }
+          ++j;
+          wA = wB;
+          cA = cB;
+          wB = j + 1 < G1 ? grp[j + 1].x : INT_MAX / 2;
+          cB = j + 1 < G1 ? cls[j + 1] : 0;
+        }
+      }
+      if (hasOwn) raise_flag(flag, bad);
+    }
+    } else if constexpr (ROLE == 1) {
     // warp w owns t1 group gA + w / nch and unknowns [cb, cb + 32 NU) of the tile;
     // lane q-th unknown = cb + lane + 32 q.  Per slice and t1 line: the normal Gram moments
     // m_a (gram_moments), then U_a += W_a(y, z) m_a for the <= 2 open t2 windows (A = j,

@@ -667,6 +667,7 @@ void prepare_ring(th_operator* op) {
 struct StageGeom {
   int nst = 0, stage_d = 0, ny_max = 0, tg = 0, tiles_per_face = 0, out_d = 0;
   size_t smem = 0;
+  bool own = false;  // line-owner consumers (stage_slide.cuh, OWN): ncw + 1 consumer warps
 };
 // restriction: one consumer warp per t1 group at u <= 64, two unknowns per lane (18 warps with one
 // unknown per lane measured 0.76 against 0.845 of the copy peak: profiles/r02_ab_restriction.txt)
@@ -695,9 +696,27 @@ bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
   const size_t extra = op->st_w.size() * 8 + 20 * 8;
   const size_t budget = size_t(227 * 1024) / size_t(minb) - 1024;
+  // Line-owner consumers: every line of a slice projected once (u <= 64; every warp owns <= 3 lines
+  // of a tile: window starts step by <= 3, the last group's window starts >= 2 after its
+  // neighbour's) where the hand-over slots fit beside a 3-stage ring (p = 9; at p = 17 they do not).
+  //   TH_ROWN=0                  one consumer warp per t1 group (5 lines each) instead (A/B, tests)
+  static const int use_own = [] { const char* e = std::getenv("TH_ROWN"); return e ? std::atoi(e) : 1; }();
+  bool own = use_own && nch == 1 && nu == 2 && L == 5 && g.tg <= ncw;
+  for (int ga = 0; own && ga < max_n; ga += g.tg) {
+    const int gb = std::min(max_n, ga + g.tg);
+    for (int i = ga; i + 1 < gb; ++i) own &= g1[i + 1].win0 - g1[i].win0 <= 3;
+    if (gb - ga >= 2) own &= g1[gb - 1].win0 - g1[gb - 2].win0 >= 2;
+  }
+  const size_t xch = size_t(ncw) * nu * 4 * 32 * 8;
   for (int nst = 3; nst >= 2; --nst) {
     const size_t smem = size_t(nst) * g.stage_d * 8 + extra + size_t(nst) * 16 + size_t(nst) * g.ny_max * 4 +
                         size_t(L) * g.ny_max + 64 * 8;
+    if (nst == 3 && own && smem + xch <= budget) {
+      g.nst = nst;
+      g.smem = smem + xch;
+      g.own = true;
+      return true;
+    }
     if (smem <= budget) {
       g.nst = nst;
       g.smem = smem;
@@ -959,13 +978,15 @@ int32_t th_apply_faces(const th_operator* op, const double* src, double* dst, co
   } while (0)
 #define TH_SLIDE(ROLE, ORDER, TENSOR, NCW, NU, MINB)                                                          \
   do {                                                                                                        \
-    auto kfn = sg.nst == 3 ? stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 3, NU, MINB>                        \
-                           : stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 2, NU, MINB>;                       \
+    auto kfn = sg.own       ? stage_slide_kernel<ROLE, ORDER, TENSOR, NCW + 1, 3, NU, MINB, true>             \
+               : sg.nst == 3 ? stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 3, NU, MINB>                      \
+                             : stage_slide_kernel<ROLE, ORDER, TENSOR, NCW, 2, NU, MINB>;                     \
     TH_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sg.smem)));           \
     const int64_t tiles = n_faces * sg.tiles_per_face;                                                       \
     const int sblocks = int(std::min<int64_t>(tiles, int64_t(num_sms()) * MINB));                             \
-    kfn<<<sblocks, (NCW + 1) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag, sg.stage_d,      \
-                                                 sg.ny_max, sg.tg, sg.tiles_per_face, sg.out_d);              \
+    kfn<<<sblocks, (NCW + (sg.own ? 2 : 1)) * 32, sg.smem, s>>>(op->dev, src, dst, faces, n_faces, u, flag,   \
+                                                                sg.stage_d, sg.ny_max, sg.tg,                 \
+                                                                sg.tiles_per_face, sg.out_d);                 \
   } while (0)
   // Kernel choice: the measured defaults (profiles/r01_ab_*.txt, r02_*); register budgets are the
   // largest occupancies at which the hot kernels do not spill.  Environment switches, read once
