@@ -96,6 +96,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   // every consumer warp used to wait out at the start of each tile while the ring stood full
   __shared__ int4 sgrp_s[kGrpSmem];
   __shared__ int scls_s[kGrpSmem];
+  __shared__ double s0_s[OWN ? 12 * 8 : 1];  // OWN: normal synthesis rows of up to 8 normal groups
+  const bool s0sm = OWN && op.G0 <= 8;
   const bool gsm = op.G1 <= kGrpSmem;
   const int4* const grp = gsm ? sgrp_s : op.grp1;
   const int* const cls = gsm ? scls_s : op.st_cls;
@@ -122,6 +124,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     // W_a(y, z) of every (t1, t2) synthesis-row class pair (host-built, trihalo.cu prepare_stage)
     for (int i = threadIdx.x; i < op.st_ncls * op.st_ncls * 100; i += blockDim.x) wtab[i] = __ldg(op.st_w + i);
     for (int i = threadIdx.x; i < 20; i += blockDim.x) wzero[i] = 0.0;
+    if (s0sm)
+      for (int i = threadIdx.x; i < op.G0 * 12; i += blockDim.x) s0_s[i] = __ldg(op.synth0 + i);
     if (gsm)
       for (int i = threadIdx.x; i < op.G1; i += blockDim.x) {
         sgrp_s[i] = __ldg(&op.grp1[i]);
@@ -328,6 +332,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     // shared-memory slot (full / empty mbarriers per slot, one writer and one reader warp each;
     // partials are written before the own group's are awaited, so the chain resolves from the
     // helper down) and warp i - 1 adds it to its own before the normal synthesis.
+    // U_a += W_a m_a for the line's four folded weights (two 16-byte broadcast loads; the tables sit
+    // on 32-byte boundaries); windows the slice does not reach are skipped (warp-uniform)
+    auto accumulate = [](const double* w, const double (&m)[NU][D], double (&U)[NU][D]) {
+      const double2 w0 = *reinterpret_cast<const double2*>(w), w1 = *reinterpret_cast<const double2*>(w + 2);
+      const double W[D] = {w0.x, w0.y, w1.x, w1.y};
+#pragma unroll
+      for (int q = 0; q < NU; ++q)
+#pragma unroll
+        for (int a = 0; a < D; ++a) U[q][a] = fma(W[a], m[q][a], U[q][a]);
+    };
     int s = 0;
     unsigned ph = 0, xin = 0, xout = 0;
     const int ncl = op.st_ncls;
@@ -394,32 +408,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
             }
             static_assert(D == 4, "order3: four degrees");
             if (ownS[k]) {
-              const double* wa = inA ? wrowO + oA + yo + k * 4 : wzero;
-              const double* wb = inB ? wrowO + oB + yo + k * 4 : wzero;
-              const double2 a0 = *reinterpret_cast<const double2*>(wa), a1 = *reinterpret_cast<const double2*>(wa + 2),
-                            b0 = *reinterpret_cast<const double2*>(wb), b1 = *reinterpret_cast<const double2*>(wb + 2);
-              const double WA[D] = {a0.x, a0.y, a1.x, a1.y}, WB[D] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-              for (int q = 0; q < NU; ++q)
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                  UA[q][a] = fma(WA[a], m[q][a], UA[q][a]);
-                  UB[q][a] = fma(WB[a], m[q][a], UB[q][a]);
-                }
+              if (inA) accumulate(wrowO + oA + yo + k * 4, m, UA);
+              if (inB) accumulate(wrowO + oB + yo + k * 4, m, UB);
             }
             if (prevS[k]) {
-              const double* wa = inA ? wrowP + oA + yp + k * 4 : wzero;
-              const double* wb = inB ? wrowP + oB + yp + k * 4 : wzero;
-              const double2 a0 = *reinterpret_cast<const double2*>(wa), a1 = *reinterpret_cast<const double2*>(wa + 2),
-                            b0 = *reinterpret_cast<const double2*>(wb), b1 = *reinterpret_cast<const double2*>(wb + 2);
-              const double WA[D] = {a0.x, a0.y, a1.x, a1.y}, WB[D] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-              for (int q = 0; q < NU; ++q)
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                  PA[q][a] = fma(WA[a], m[q][a], PA[q][a]);
-                  PB[q][a] = fma(WB[a], m[q][a], PB[q][a]);
-                }
+              if (inA) accumulate(wrowP + oA + yp + k * 4, m, PA);
+              if (inB) accumulate(wrowP + oB + yp + k * 4, m, PB);
             }
           }
         }
@@ -457,7 +451,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
             const int t1 = grp[gO].z, t2 = grp[j].z;
             if (t1 >= fr.lo1 && t1 < fr.lo1 + p && t2 >= fr.lo2 && t2 < fr.lo2 + p) {
               const int4 G0 = fr.g0 == 0 ? G0c : __ldg(&op.grp0[fr.g0]);
-              const double* s0 = op.synth0 + fr.g0 * 12;
+              const double* s0 = (s0sm ? s0_s : op.synth0) + fr.g0 * 12;
               double* const ob = dst + fr.dst + int64_t(t1 - fr.lo1) * fr.d1 + int64_t(t2 - fr.lo2) * fr.d2 + lane;
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
@@ -465,7 +459,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
                 if (c < G0.w && t0 >= fr.lo0 && t0 < fr.hi0) {
                   double S0[D];
 #pragma unroll
-                  for (int a = 0; a < D; ++a) S0[a] = __ldg(s0 + c * 4 + a);
+                  for (int a = 0; a < D; ++a) S0[a] = s0[c * 4 + a];
 #pragma unroll
                   for (int q = 0; q < NU; ++q) {
                     double o = 0.0;

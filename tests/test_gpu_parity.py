@@ -393,7 +393,8 @@ def test_pool_transposed_layout(th, scheme, p):
 
 @pytest.mark.parametrize("env", ({"TH_GRAM": "3"}, {"TH_TILE": "0"}, {"TH_TILE3": "0"},
                                  {"TH_TILE": "0", "TH_GRAM": "0"}, {"TH_RING": "15"},
-                                 {"TH_RING": "15", "TH_RING_NA": "3", "TH_RING_R": "6"}, {"TH_RING": "0"}))
+                                 {"TH_RING": "15", "TH_RING_NA": "3", "TH_RING_R": "6"}, {"TH_RING": "0"},
+                                 {"TH_ROWN": "0"}))
 def test_alternative_kernel_paths(th, env):
     """Kernel choices are read once per process from the environment; re-run the
     parity tests in a child process with the alternative paths (the per-warp order3
@@ -401,7 +402,8 @@ def test_alternative_kernel_paths(th, env):
     the per-warp slide for order3 interpolation instead of the two-phase order3 tiles; the
     fixed-window kernels with neither tiles nor Gram slides; the slice ring (ring_interp.cuh)
     for every interpolation (Gram and d-linear), also with 3 A warps and the smallest ring; the
-    per-warp slide instead of the slice ring at p = 17)."""
+    per-warp slide instead of the slice ring at p = 17; the staged order3 restriction with one
+    consumer warp per t1 group instead of the line owners)."""
     import os
     import subprocess
     import sys
