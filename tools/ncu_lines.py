@@ -40,6 +40,6 @@ for r in csv.reader(io.StringIO(out)):
 tot_s = sum(v[0] for v in agg.values()) or 1
 tot_i = sum(v[1] for v in agg.values()) or 1
 print(f"samples {tot_s}  warp instructions {tot_i}")
-for (fn, ln), (s, i, src, why) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+for (fn, ln), (s, i, src, why) in sorted(agg.items(), key=lambda kv: -kv[1][1 if "--by-inst" in sys.argv else 0])[:top]:
     reasons = " ".join(f"{k}:{100 * v / max(s, 1):.0f}" for k, v in why.most_common(3))
     print(f"{100 * s / tot_s:5.1f}% stall {100 * i / tot_i:5.1f}% inst  {fn}:{ln:>4}  {src[:60]:60}  [{reasons}]")
