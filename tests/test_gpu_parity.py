@@ -459,6 +459,15 @@ def test_pool_restrict_order3_unknown_counts(th, u, p):
         assert rel(out[f], want) <= TOL, (u, p, f, rel(out[f], want))
 
 
+@pytest.mark.parametrize("p", (5, 6, 7, 8, 10, 11, 12, 13, 16))
+def test_pool_restrict_order3_patch_sizes(th, p):
+    """Staged order3 restriction across patch sizes: the line-owner consumers' line ranges, the
+    helper warp and the partial hand-over for every tile shape (one tile of p groups at p <= 9,
+    two tiles of p / 2 groups above; clipped first / last windows; p = 17 keeps one warp per
+    group and is covered above)."""
+    test_pool_restrict_order3_unknown_counts(th, 59, p)
+
+
 @pytest.mark.parametrize("scheme", ("tensor_linear", "order2", "order3"))
 def test_interp_into_fine_patches(th, scheme):
     """Interpolation written into the fine patches' reference target cells equals the slab run."""
