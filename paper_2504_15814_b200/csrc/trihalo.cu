@@ -695,7 +695,8 @@ bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   // 63 - u doubles beyond a cell (never stored), covered by the regions that follow the stages
   g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
   const size_t extra = op->st_w.size() * 8 + 20 * 8;
-  const size_t budget = size_t(227 * 1024) / size_t(minb) - 1024;
+  // (dynamic shared memory: the opt-in maximum less the kernels' static tables)
+  const size_t budget = size_t(227 * 1024) / size_t(minb) - 3072;
   // Line-owner consumers: every line of a slice projected once (u <= 64; every warp owns <= 3 lines
   // of a tile: window starts step by <= 3, the last group's window starts >= 2 after its
   // neighbour's) where the hand-over slots fit beside a 3-stage ring (p = 9; at p = 17 they do not).
