@@ -21,6 +21,13 @@
 //       Q_ab(j) = sum_z K_{a+b}(j, z) T_ab(w_j + z),  K_d(j, z) = sum_{c <= 3-d} S2_j[c] P_c(z),
 //       out_i   = sum_a S0_i[a] sum_b S1[b] Q_ab,
 //     the two open windows' Q living in registers (NU = 2 unknowns per lane).
+//   OWN (u <= 64, tiles of <= NCW - 1 groups, 3-stage ring + hand-over slots fit: p <= 16): the
+//     t1 windows are 5 lines long and step by 3, so one warp per t1 group projects 2 of every 3
+//     lines twice.  The line-owner consumers project every line once: warp i owns the lines
+//     [w_i, w_{i+1}) (<= 3 per slice), accumulates them into its own group's windows and -- where a
+//     line also lies in window i - 1 -- into a partial it keeps for the previous group, handed over
+//     through a shared-memory slot when a t2 window completes (config 5: 0.85 -> 0.925 of the copy
+//     peak; profiles/r02_ab_restriction.txt, entries 10-11).
 //   (An interpolation consumer on the same producer -- ROLE 0, with TMA bulk stores of the
 //   output -- measured no faster than the per-warp slide and was removed in round 2;
 //   profiles/r01_ab_stage.txt.)
