@@ -693,7 +693,7 @@ bool stage_geometry(const th_operator* op, int u, int minb, StageGeom& g) {
   }
   // stage rows hold runs of u-double cells widened to 16-byte boundaries; lanes past u read up to
   // 63 - u doubles beyond a cell (never stored), covered by the regions that follow the stages
-  g.stage_d = (L * g.ny_max * (u + 3) + 1) & ~1;
+  g.stage_d = (L * g.ny_max * ((u + 3) & ~1) + 1) & ~1;  // cell slots of round_even(u + 2) doubles
   const size_t extra = op->st_w.size() * 8 + 20 * 8;
   // (dynamic shared memory: the opt-in maximum less the kernels' static tables)
   const size_t budget = size_t(227 * 1024) / size_t(minb) - 3072;

@@ -25,13 +25,15 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 import paper_2504_15814_b200 as th
 from paper_2504_15814_b200 import faces as F
 
 K_HALO = 3
-U = 59
+U = int(os.environ.get("TH_BENCH_U", "59"))  # 59 (BASELINE); the override is for layout A/B runs only
 
 
 @dataclass
